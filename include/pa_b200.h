@@ -1,0 +1,99 @@
+/*
+ * pa_b200.h -- C ABI of the B200-native modular-arithmetic PA hash.
+ *
+ * The hash (reference: modpa, arxiv/paper_1910_04429) is
+ *     y = floor(((c * x + d) mod 2^n) / 2^(n - r)),   c odd,
+ * over n-bit blocks x and a per-block seed (c, d).  Blocks are byte strings
+ * of ceil(n/8) bytes in the reference's layout: bit i of the block is bit i
+ * of its integer value, bytes least-significant-first (LSF, default) or
+ * most-significant-first (MSF), zero padded at the most-significant end
+ * (pkg/src/modpa/pa.py:8-11, 111-132).  Outputs are ceil(r/8) bytes per
+ * block in the same byte order.
+ *
+ * The reference has no FFI: its seam is the Python functions listed at each
+ * entry point below.  This header is what the Python drop-in
+ * (paper_1910_04429_b200/pa.py, bignum.py) binds with ctypes; see
+ * INTEGRATION.md for the binding a modpa maintainer would add.
+ *
+ * Conventions: every function returns PAB_OK (0) or a negative PAB_E* code
+ * and never throws; pab_last_error() returns a thread-local message for the
+ * last failure on the calling thread.  Device pointers must be CUDA device
+ * memory of the current device; `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  All entry points are reentrant; tables are built once
+ * per (device, transform length) under a mutex and never freed.
+ */
+#ifndef PA_B200_H
+#define PA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAB_OK 0
+#define PAB_EINVAL (-1) /* bad argument (message in pab_last_error) */
+#define PAB_ENOMEM (-2) /* device allocation failed -> Python MemoryError */
+#define PAB_ECUDA (-3)  /* any other CUDA error */
+#define PAB_ERANGE (-4) /* size beyond the exact-convolution bound */
+
+#define PAB_ORDER_LSF 0 /* WordOrder.LEAST_SIGNIFICANT_FIRST, pkg/src/modpa/bignum.py:27-31 */
+#define PAB_ORDER_MSF 1 /* WordOrder.MOST_SIGNIFICANT_FIRST */
+
+/* ABI version (major*100 + minor). */
+int pab_version(void);
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* pab_last_error(void);
+/* Largest block size n (bits) the exact three-prime convolution supports. */
+uint64_t pab_max_bits(void);
+
+/* Transform geometry chosen for an n-bit hash: L = 2^lg = 2^lgR * 2^lgC. */
+int pab_plan_info(uint64_t n_bits, int* lg, int* lg_rows, int* lg_cols);
+
+/*
+ * Device workspace needed to hash `batch` n-bit blocks in one pass.
+ * pab_hash_batch processes larger batches in chunks that fit the workspace
+ * it is given (at least one block must fit).
+ */
+size_t pab_hash_workspace_bytes(uint64_t n_bits, uint32_t batch);
+
+/*
+ * Batched, device-resident hash.  Replaces, per block i,
+ *   export_block(compress(import_block(x_i), HashSeed(c_i, d_i, n), r))
+ * i.e. pkg/src/modpa/pa.py:175-190 (compress) with the byte layout of
+ * import_block/export_block (pa.py:111-132).
+ *   x, c, d : device, block i at offset i*in_stride, ceil(n/8) bytes each
+ *   out     : device, block i at offset i*out_stride, ceil(r/8) bytes each
+ * Requirements (checked in Python by the drop-in, as in the reference):
+ * 1 <= r <= n <= pab_max_bits(); c odd; bits >= n of x, c, d are ignored.
+ */
+int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t in_stride,
+                   uint64_t n_bits, uint64_t r_bits, uint32_t batch, int byte_order,
+                   uint8_t* out, uint64_t out_stride, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
+/*
+ * Host-buffer hash on `device` (the drop-in compress / pa_round path,
+ * pkg/src/modpa/pa.py:175-217): copies x, c, d (batch*ceil(n/8) bytes each,
+ * contiguous) host->device, hashes, copies batch*ceil(r/8) bytes back.
+ * Uses a per-device cached workspace and stream; blocks until done.
+ */
+int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
+                  uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device);
+
+/*
+ * Exact product of two naturals given as LSF byte strings (bignum.mul,
+ * pkg/src/modpa/bignum.py:194-231): out receives a_bytes + b_bytes LSF bytes.
+ */
+size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes);
+int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes, uint8_t* out,
+            void* workspace, size_t workspace_bytes, void* stream);
+int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes,
+                 uint8_t* out, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PA_B200_H */

@@ -1,0 +1,120 @@
+"""ctypes binding of the C ABI declared in include/pa_b200.h.
+
+The library is built in-tree (``paper_1910_04429_b200/_lib/libpa_b200.so``,
+see csrc/Makefile and ``__graft_entry__.build``).  There is no CPU fallback:
+if the library is missing or CUDA is unavailable every entry point raises.
+Error codes map onto the reference's Python conventions: PAB_EINVAL and
+PAB_ERANGE -> ValueError, PAB_ENOMEM -> MemoryError (what
+``bench.run_bench`` catches, pkg/src/modpa/bench.py:162-173), anything else
+-> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libpa_b200.so")
+
+PAB_OK = 0
+PAB_EINVAL = -1
+PAB_ENOMEM = -2
+PAB_ECUDA = -3
+PAB_ERANGE = -4
+ORDER_LSF = 0
+ORDER_MSF = 1
+
+# name -> (restype, argtypes); every symbol include/pa_b200.h declares
+_u8p = ctypes.c_void_p
+SIGNATURES = {
+    "pab_version": (ctypes.c_int, []),
+    "pab_last_error": (ctypes.c_char_p, []),
+    "pab_max_bits": (ctypes.c_uint64, []),
+    "pab_plan_info": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "pab_hash_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
+    "pab_hash_batch": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _u8p,
+                                      ctypes.c_uint64, _u8p, ctypes.c_size_t, _u8p]),
+    "pab_hash_host": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
+                                     ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_int]),
+    "pab_mul_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint64]),
+    "pab_mul": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p, _u8p,
+                               ctypes.c_size_t, _u8p]),
+    "pab_mul_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
+                                    ctypes.c_int]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is missing or cannot run here (no CPU fallback)."""
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree library (raises NativeUnavailable if it is not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailable(
+                    f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                    " (there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def check(rc: int) -> None:
+    if rc == PAB_OK:
+        return
+    msg = load().pab_last_error().decode(errors="replace")
+    if rc in (PAB_EINVAL, PAB_ERANGE):
+        raise ValueError(msg)
+    if rc == PAB_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"CUDA error in pa_b200: {msg}")
+
+
+def _device() -> int:
+    import torch  # plumbing only: device selection follows torch's current device
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible (there is no CPU fallback)")
+    return torch.cuda.current_device()
+
+
+def hash_host(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
+              order: int = ORDER_LSF, device: int | None = None) -> bytes:
+    """Hash `batch` blocks given as contiguous host byte strings; returns output bytes."""
+    lib = load()
+    dev = _device() if device is None else device
+    out = ctypes.create_string_buffer(batch * ((r + 7) // 8))
+    check(lib.pab_hash_host(x, c, d, n, r, batch, order, out, dev))
+    return out.raw
+
+
+def mul_host(a: bytes, b: bytes, device: int | None = None) -> bytes:
+    lib = load()
+    dev = _device() if device is None else device
+    out = ctypes.create_string_buffer(len(a) + len(b))
+    check(lib.pab_mul_host(a, len(a), b, len(b), out, dev))
+    return out.raw
+
+
+def plan_info(n: int) -> tuple[int, int, int]:
+    lib = load()
+    lg, lr, lc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    check(lib.pab_plan_info(n, ctypes.byref(lg), ctypes.byref(lr), ctypes.byref(lc)))
+    return lg.value, lr.value, lc.value
+
+
+def max_bits() -> int:
+    return int(load().pab_max_bits())

@@ -1,0 +1,83 @@
+// Word-size modular arithmetic for the three-prime NTT (sm_100a integer pipe).
+//
+// The reference multiplies in the Fermat ring Z/(2^N'+1) with shift twiddles
+// (pkg/src/modpa/ntt.py:123-160).  On B200 the product is instead formed as
+// an exact cyclic convolution of 32-bit words over three primes p_i < 2^30
+// (CRT-recombined in the carry kernel), so every operation here is on u32
+// registers: Shoup multiplication for known twiddles, Montgomery reduction
+// for products of two data values, and Harvey-style lazy butterflies that
+// keep values in [0, 2p) or [0, 4p) instead of fully reducing.
+#pragma once
+#include <cstdint>
+
+namespace pab {
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+constexpr int kNumPrimes = 3;
+// p_i = k_i * 2^23 + 1, p_i < 2^30 (so 4p < 2^32); product ~ 2^89.35.
+constexpr u32 kPrimes[kNumPrimes] = {998244353u, 897581057u, 880803841u};
+constexpr int kMaxLg = 23;        // 2-adicity common to all three primes
+constexpr int kTwN = 4096;        // largest in-CTA sub-transform
+constexpr int kTwLg = 12;
+
+struct PrimeInfo {
+  u32 p;
+  u32 two_p;
+  u32 p_mont;   // -p^{-1} mod 2^32
+  u32 one_sh;   // floor(2^32 / p): Shoup companion of w = 1
+};
+
+#ifdef __CUDACC__
+// Shoup multiplication a*w mod p with precomputed wp = floor(w*2^32/p).
+// Any a < 2^32; result in [0, 2p).
+__device__ __forceinline__ u32 shoup(u32 a, u32 w, u32 wp, u32 p) {
+  u32 q = __umulhi(a, wp);
+  return a * w - q * p;
+}
+__device__ __forceinline__ u32 shoup(u32 a, uint2 w, u32 p) { return shoup(a, w.x, w.y, p); }
+
+// [0, 2m) -> [0, m) (unsigned wrap makes the min pick the right branch).
+__device__ __forceinline__ u32 red(u32 a, u32 m) { return min(a, a - m); }
+
+// Montgomery product a*b*2^-32 mod p; a*b < 4p^2 gives a result in [0, 2p).
+__device__ __forceinline__ u32 montmul(u32 a, u32 b, u32 p, u32 p_mont) {
+  u64 t = (u64)a * b;
+  u32 lo = (u32)t, hi = (u32)(t >> 32);
+  u32 m = lo * p_mont;
+  u32 mh = __umulhi(m, p);
+  return hi + mh + (lo != 0u ? 1u : 0u);
+}
+
+// Gentleman-Sande (DIF) butterfly: x, y in [0, 2p) -> x+y, (x-y)*w, both [0, 2p).
+__device__ __forceinline__ void dif_bfly(u32& x, u32& y, uint2 w, u32 p, u32 two_p) {
+  u32 s = red(x + y, two_p);
+  u32 d = x - y + two_p;
+  y = shoup(d, w, p);
+  x = s;
+}
+// DIF butterfly with twiddle 1.
+__device__ __forceinline__ void dif_bfly1(u32& x, u32& y, u32 two_p) {
+  u32 s = red(x + y, two_p);
+  u32 d = x - y + two_p;
+  y = red(d, two_p);
+  x = s;
+}
+// Cooley-Tukey (DIT) butterfly: x in [0, 4p), y < 2^32 -> x+w*y, x-w*y in [0, 4p).
+__device__ __forceinline__ void dit_bfly(u32& x, u32& y, uint2 w, u32 p, u32 two_p) {
+  u32 a = red(x, two_p);
+  u32 t = shoup(y, w, p);
+  x = a + t;
+  y = a - t + two_p;
+}
+// DIT butterfly with twiddle 1 (y must be < 4p).
+__device__ __forceinline__ void dit_bfly1(u32& x, u32& y, u32 two_p) {
+  u32 a = red(x, two_p);
+  u32 t = red(y, two_p);
+  x = a + t;
+  y = a - t + two_p;
+}
+#endif
+
+}  // namespace pab
