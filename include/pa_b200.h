@@ -92,6 +92,15 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
 int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes,
                  uint8_t* out, int device);
 
+/*
+ * Optional per-kernel timing: while enabled, CUDA events are recorded on the
+ * launching stream around every kernel.  pab_profile_collect synchronizes on
+ * them, aggregates by kernel name (static strings) into the caller's arrays
+ * (at most `cap` names) and clears the record; returns the number of names.
+ */
+void pab_profile_enable(int enable);
+int pab_profile_collect(const char** names, int* counts, double* total_ms, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,10 @@ SIGNATURES = {
                                ctypes.c_size_t, _u8p]),
     "pab_mul_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
                                     ctypes.c_int]),
+    "pab_profile_enable": (None, [ctypes.c_int]),
+    "pab_profile_collect": (ctypes.c_int, [ctypes.POINTER(ctypes.c_char_p),
+                                           ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
 }
 
 _lib = None
@@ -114,6 +118,21 @@ def plan_info(n: int) -> tuple[int, int, int]:
     lg, lr, lc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     check(lib.pab_plan_info(n, ctypes.byref(lg), ctypes.byref(lr), ctypes.byref(lc)))
     return lg.value, lr.value, lc.value
+
+
+def profile_enable(on: bool = True) -> None:
+    """Record CUDA events around every kernel launch (see pab_profile_enable)."""
+    load().pab_profile_enable(1 if on else 0)
+
+
+def profile_collect() -> dict[str, tuple[int, float]]:
+    """{kernel: (launches, total_ms)} since the last collect (synchronizes)."""
+    cap = 32
+    names = (ctypes.c_char_p * cap)()
+    counts = (ctypes.c_int * cap)()
+    ms = (ctypes.c_double * cap)()
+    k = load().pab_profile_collect(names, counts, ms, cap)
+    return {names[i].decode(): (counts[i], ms[i]) for i in range(k)}
 
 
 def max_bits() -> int:

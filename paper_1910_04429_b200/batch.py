@@ -1,0 +1,126 @@
+"""Batched PA hashing on one GPU: device-resident and host-streamed paths.
+
+This is the "batched scheduler" of the north star (host
+scheduler row): many independent blocks per launch (grid dimension = block),
+per-stream workspaces, pinned host staging, and H2D / compute / D2H of
+successive chunks overlapped on separate CUDA streams.  It generalises the
+reference's sequential batch loop (pkg/src/modpa/bench.py:256-262).
+
+PyTorch is used only as plumbing (device memory, pinned host memory, streams
+and events); every byte of hashing runs in the C-ABI library.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class HashEngine:
+    """Hash batches of n-bit blocks down to r bits on one CUDA device.
+
+    Inputs are uint8 tensors of shape [batch, ceil(n/8)] (x, c, d) in the
+    reference's serialized layout; outputs [batch, ceil(r/8)].
+    """
+
+    def __init__(self, n: int, r: int, *, device: int | torch.device | None = None,
+                 order: int = _native.ORDER_LSF, max_batch: int = 64,
+                 max_workspace: int = 4 << 30):
+        if not 1 <= r <= n:
+            raise ValueError(f"output length r={r} must satisfy 1 <= r <= n={n}")
+        self.lib = _native.load()
+        if not torch.cuda.is_available():
+            raise _native.NativeUnavailable("no CUDA device (there is no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.n, self.r, self.order = n, r, order
+        self.nbytes, self.rbytes = (n + 7) // 8, (r + 7) // 8
+        chunk = max(1, max_batch)
+        while chunk > 1 and self.lib.pab_hash_workspace_bytes(n, chunk) > max_workspace:
+            chunk //= 2
+        self.chunk = chunk
+        self.ws_bytes = int(self.lib.pab_hash_workspace_bytes(n, chunk))
+        if self.ws_bytes == 0:
+            _native.check(_native.PAB_EINVAL)
+        self._ws = {}
+
+    def _workspace(self, stream: torch.cuda.Stream) -> torch.Tensor:
+        key = stream.cuda_stream
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
+
+    def hash_device(self, x: torch.Tensor, c: torch.Tensor, d: torch.Tensor,
+                    out: torch.Tensor | None = None,
+                    stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Hash device-resident blocks (enqueued on `stream`, asynchronous)."""
+        b = x.shape[0]
+        for t in (x, c, d):
+            if t.device != self.device or t.dtype != torch.uint8 or t.dim() != 2:
+                raise ValueError("x, c, d must be 2-D uint8 tensors on the engine's device")
+            if t.shape[0] != b or t.shape[1] < self.nbytes or t.stride(1) != 1:
+                raise ValueError("x, c, d must be [batch, >= ceil(n/8)] with unit byte stride")
+        if not (x.stride(0) == c.stride(0) == d.stride(0)):
+            raise ValueError("x, c, d must share one row stride")
+        st = stream or torch.cuda.current_stream(self.device)
+        if out is None:
+            out = torch.empty((b, self.rbytes), dtype=torch.uint8, device=self.device)
+        ws = self._workspace(st)
+        _native.check(self.lib.pab_hash_batch(
+            _ptr(x), _ptr(c), _ptr(d), x.stride(0), self.n, self.r, b, self.order,
+            _ptr(out), out.stride(0), _ptr(ws), self.ws_bytes, ctypes.c_void_p(st.cuda_stream)))
+        return out
+
+    def hash_host(self, x: torch.Tensor, c: torch.Tensor, d: torch.Tensor,
+                  out: torch.Tensor | None = None, streams: int = 2,
+                  chunk: int | None = None) -> torch.Tensor:
+        """End-to-end from (pinned) host tensors: H2D, hash, D2H, overlapped.
+
+        Chunks of blocks rotate over `streams` CUDA streams so the copy of
+        chunk i+1 overlaps the hashing of chunk i.  Returns host [batch, ceil(r/8)].
+        """
+        b = x.shape[0]
+        if out is None:
+            out = torch.empty((b, self.rbytes), dtype=torch.uint8, pin_memory=True)
+        chunk = chunk or self.chunk
+        sts = self._streams(streams)
+        bufs = self._io_buffers(len(sts), chunk)
+        cur = torch.cuda.current_stream(self.device)
+        for s in sts:
+            s.wait_stream(cur)
+        for i, b0 in enumerate(range(0, b, chunk)):
+            k = i % len(sts)
+            st = sts[k]
+            dx, dc, dd, dout = bufs[k]
+            nb = min(chunk, b - b0)
+            with torch.cuda.stream(st):
+                dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
+                dc[:nb].copy_(c[b0:b0 + nb], non_blocking=True)
+                dd[:nb].copy_(d[b0:b0 + nb], non_blocking=True)
+                self.hash_device(dx[:nb], dc[:nb], dd[:nb], dout[:nb], stream=st)
+                out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
+        for s in sts:
+            cur.wait_stream(s)
+        return out
+
+    def _streams(self, k: int):
+        if not hasattr(self, "_sts") or len(self._sts) != k:
+            self._sts = [torch.cuda.Stream(self.device) for _ in range(k)]
+        return self._sts
+
+    def _io_buffers(self, k: int, chunk: int):
+        key = (k, chunk)
+        if getattr(self, "_io_key", None) != key:
+            mk = lambda w: torch.empty((chunk, w), dtype=torch.uint8, device=self.device)  # noqa: E731
+            self._io = [(mk(self.nbytes), mk(self.nbytes), mk(self.nbytes), mk(self.rbytes))
+                        for _ in range(k)]
+            self._io_key = key
+        return self._io

@@ -21,6 +21,8 @@
 
 namespace pab {
 void set_kernel_attrs();
+void profile_enable(bool enable);
+int profile_collect(const char** names, int* counts, double* ms, int cap);
 }
 
 using namespace pab;
@@ -546,6 +548,12 @@ int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t 
     CK(cudaMemcpyAsync(out, dout, a_bytes + b_bytes, cudaMemcpyDeviceToHost, h.stream), "D2H");
   CK(cudaStreamSynchronize(h.stream), "synchronize");
   return PAB_OK;
+}
+
+void pab_profile_enable(int enable) { profile_enable(enable != 0); }
+
+int pab_profile_collect(const char** names, int* counts, double* total_ms, int cap) {
+  return profile_collect(names, counts, total_ms, cap);
 }
 
 }  // extern "C"

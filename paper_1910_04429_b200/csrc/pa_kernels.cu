@@ -14,7 +14,85 @@
 #include "pa_kernels.cuh"
 #include "ntt_panel.cuh"
 
+#include <mutex>
+#include <string>
+#include <vector>
+
 namespace pab {
+
+// ---------------------------------------------------------------------------
+// Optional per-kernel event timing (pab_profile_*): events are recorded on the
+// launching stream around every kernel while enabled.
+namespace prof {
+struct Rec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+static std::mutex mu;
+static bool on = false;
+static std::vector<Rec> recs;
+static std::vector<cudaEvent_t> pool;
+static cudaEvent_t get_ev() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct Scope {
+  bool active;
+  Rec r;
+  cudaStream_t st;
+  Scope(const char* name, cudaStream_t s) : active(false), st(s) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!on) return;
+    active = true;
+    r.name = name;
+    r.a = get_ev();
+    r.b = get_ev();
+    cudaEventRecord(r.a, st);
+  }
+  ~Scope() {
+    if (!active) return;
+    cudaEventRecord(r.b, st);
+    std::lock_guard<std::mutex> lk(mu);
+    recs.push_back(r);
+  }
+};
+}  // namespace prof
+
+void profile_enable(bool enable) {
+  std::lock_guard<std::mutex> lk(prof::mu);
+  prof::on = enable;
+}
+// Aggregates by kernel name: returns number of distinct names written.
+int profile_collect(const char** names, int* counts, double* ms, int cap) {
+  std::lock_guard<std::mutex> lk(prof::mu);
+  int nn = 0;
+  for (auto& r : prof::recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    int i = 0;
+    while (i < nn && std::string(names[i]) != r.name) ++i;
+    if (i == nn) {
+      if (nn == cap) continue;
+      names[nn] = r.name;
+      counts[nn] = 0;
+      ms[nn] = 0.0;
+      ++nn;
+    }
+    counts[i] += 1;
+    ms[i] += t;
+    prof::pool.push_back(r.a);
+    prof::pool.push_back(r.b);
+  }
+  prof::recs.clear();
+  return nn;
+}
 
 __constant__ PrimeInfo c_primes[kNumPrimes];
 __constant__ CrtConst c_crt;
@@ -81,6 +159,7 @@ void launch_pack(const uint8_t* in, long long in_stride_bytes, long long n_bits,
   long long gx = (kw + threads - 1) / threads;
   if (gx > 4096) gx = 4096;
   if (gx < 1) gx = 1;
+  prof::Scope ps_("k_pack", st);
   k_pack<<<dim3((unsigned)gx, batch), threads, 0, st>>>(in, in_stride_bytes, n_bits, msf, words,
                                                         word_stride, kw);
 }
@@ -92,6 +171,7 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
   long long gx = (mb + threads - 1) / threads;
   if (gx > 4096) gx = 4096;
   if (gx < 1) gx = 1;
+  prof::Scope ps_("k_unpack", st);
   k_unpack<<<dim3((unsigned)gx, batch), threads, 0, st>>>(words, word_stride, m_bits, msf, out,
                                                           out_stride_bytes);
 }
@@ -438,23 +518,34 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   if (job.lgR == 0) {
     const int lnr = 0;
     const size_t sm = (size_t)tm_stride(job.lgC) * (2 << lnr) * 4;
+    prof::Scope ps_("k_row_single", st);
     k_row<<<dim3(1, kNumPrimes, job.batch), threads, sm, st>>>(job, tab, lnr);
     return;
   }
   const int lct = col_lct(job.lgR, job.lgC);
   const size_t smc = (size_t)panel_words(job.lgR, lct) * 4;
-  k_col_fwd<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(job, tab,
-                                                                                          lct);
+  {
+    prof::Scope ps_("k_col_fwd", st);
+    k_col_fwd<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(
+        job, tab, lct);
+  }
   int lnr = 13 - job.lgC;  // ~8K words (A+X) per CTA
   if (lnr < 0) lnr = 0;
   if (lnr > job.lgR) lnr = job.lgR;
   const size_t smr = (size_t)tm_stride(job.lgC) * (2 << lnr) * 4;
-  k_row<<<dim3(1u << (job.lgR - lnr), kNumPrimes, job.batch), threads, smr, st>>>(job, tab, lnr);
-  k_col_inv<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc, st>>>(job, tab,
-                                                                                      lct);
+  {
+    prof::Scope ps_("k_row", st);
+    k_row<<<dim3(1u << (job.lgR - lnr), kNumPrimes, job.batch), threads, smr, st>>>(job, tab, lnr);
+  }
+  {
+    prof::Scope ps_("k_col_inv", st);
+    k_col_inv<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc, st>>>(job, tab,
+                                                                                        lct);
+  }
 }
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
+  prof::Scope ps_("k_carry", st);
   k_carry<<<dim3(job.tiles, job.batch), kCarryThreads, 0, st>>>(job);
 }
 
