@@ -263,6 +263,8 @@ int lg_for(u64 len) {  // smallest lg with 2^lg >= len, at least 6
   return lg;
 }
 
+constexpr u64 kMaxChunk = 16384;  // blocks per launch (grid.y/z <= 65535)
+
 u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 u64 round_up(u64 a, u64 b) { return ceil_div(a, b) * b; }
 
@@ -384,7 +386,7 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   const PlanTables tab = tables_of(ds, pl);
   cudaStream_t st = (cudaStream_t)stream;
   // blocks per chunk that fit the workspace
-  u64 chunk = batch;
+  u64 chunk = batch < kMaxChunk ? batch : kMaxChunk;  // grid y/z limits
   while (chunk > 0 && layout_for(g.K, g.lg, g.K, g.mw, chunk).total > workspace_bytes) chunk /= 2;
   if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
   const int msf = byte_order == PAB_ORDER_MSF;
