@@ -17,10 +17,10 @@
 #include <vector>
 
 #include "../../include/pa_b200.h"
+#include "ntt_core.cuh"
 #include "pa_kernels.cuh"
 
 namespace pab {
-void set_kernel_attrs();
 void profile_enable(bool enable);
 int profile_collect(const char** names, int* counts, double* ms, int cap);
 }
@@ -62,26 +62,6 @@ u64 powmod(u64 a, u64 e, u64 m) {
 u32 inv_mod(u32 a, u32 p) { return (u32)powmod(a, p - 2, p); }
 u32 shoup_of(u32 w, u32 p) { return (u32)(((u64)w << 32) / p); }
 
-u32 primitive_root(u32 p) {
-  std::vector<u64> fac;
-  u64 m = p - 1;
-  for (u64 q = 2; q * q <= m; ++q)
-    if (m % q == 0) {
-      fac.push_back(q);
-      while (m % q == 0) m /= q;
-    }
-  if (m > 1) fac.push_back(m);
-  for (u32 g = 2;; ++g) {
-    bool ok = true;
-    for (u64 q : fac)
-      if (powmod(g, (p - 1) / q, p) == 1) {
-        ok = false;
-        break;
-      }
-    if (ok) return g;
-  }
-}
-
 PrimeInfo prime_info(u32 p) {
   PrimeInfo pi;
   pi.p = p;
@@ -93,11 +73,12 @@ PrimeInfo prime_info(u32 p) {
   return pi;
 }
 
-// root of unity of order 2^k (dir 1: its inverse)
-u32 root_pow2(u32 p, int k, int dir) {
-  const u32 g = primitive_root(p);
-  u32 w = (u32)powmod(g, (u64)(p - 1) >> k, p);
-  return dir ? inv_mod(w, p) : w;
+// root of unity of order 2^k (dir 1: its inverse); the same roots the device
+// code derives at compile time (ntt_core.cuh: croot)
+u32 root_pow2(int prime, int k, int dir) {
+  const u32 p = kPrimes[prime];
+  const u32 w23 = dir ? kIRoot23[prime] : kRoot23[prime];
+  return (u32)powmod(w23, (u64)1 << (kMaxLg - k), p);
 }
 
 // ------------------------------------------------------------ device state
@@ -105,6 +86,7 @@ struct Plan {
   int lg, lgR, lgC;
   u32* tlo_m = nullptr;
   uint2* thi = nullptr;
+  uint2* g = nullptr;
   u32 scale[kNumPrimes], scale_sh[kNumPrimes];
 };
 
@@ -133,6 +115,12 @@ int ensure_device(int dev, DevState** out) {
   if (!slot) slot.reset(new DevState());
   DevState* ds = slot.get();
   if (!ds->ready) {
+    for (int i = 0; i < kNumPrimes; ++i) {  // the compiled-in roots must be primitive 2^23-th
+      const u32 p = kPrimes[i];
+      if (powmod(kRoot23[i], (u64)1 << (kMaxLg - 1), p) != p - 1 ||
+          (u64)kRoot23[i] * kIRoot23[i] % p != 1)
+        return fail(PAB_ECUDA, "internal: bad root-of-unity constants");
+    }
     PrimeInfo pis[kNumPrimes];
     for (int i = 0; i < kNumPrimes; ++i) pis[i] = prime_info(kPrimes[i]);
     CrtConst crt;
@@ -157,7 +145,7 @@ int ensure_device(int dev, DevState** out) {
         t[0] = make_uint2(1, shoup_of(1, p));
         for (int s = 0; s < kTwLg; ++s) {
           const int h = 1 << s;
-          const u32 w = root_pow2(p, s + 1, dir);
+          const u32 w = root_pow2(i, s + 1, dir);
           u64 x = 1;
           for (int e = 0; e < h; ++e) {
             t[h + e] = make_uint2((u32)x, shoup_of((u32)x, p));
@@ -205,11 +193,22 @@ int get_plan(DevState* ds, int lg, const Plan** out) {
   split_lg(lg, &pl.lgR, &pl.lgC);
   std::vector<u32> tlo((size_t)kNumPrimes * 2 * kTwN, 0);
   std::vector<uint2> thi((size_t)kNumPrimes * 2 * kTwN, make_uint2(0, 0));
+  std::vector<uint2> gt((size_t)kNumPrimes * 2 * kTwN, make_uint2(0, 0));
+  // row-pass twiddle step: w_L^(k1 * 2^slo0), slo0 = lowest stage of the row's top pass
+  const int slo0 = pass_plan(pl.lgC).slo[0];
   for (int i = 0; i < kNumPrimes; ++i) {
     const u32 p = kPrimes[i];
     const u64 r32 = ((u64)1 << 32) % p;
     for (int dir = 0; dir < 2; ++dir) {
-      const u32 wL = root_pow2(p, lg, dir);
+      const u32 wL = root_pow2(i, lg, dir);
+      if (pl.lgR > 0) {
+        const u64 gstep = powmod(wL, (u64)1 << slo0, p);
+        u64 y = 1;
+        for (int k = 0; k < (1 << pl.lgR); ++k) {
+          gt[((size_t)i * 2 + dir) * kTwN + k] = make_uint2((u32)y, shoup_of((u32)y, p));
+          y = y * gstep % p;
+        }
+      }
       u64 x = 1;
       for (int e = 0; e < kTwN; ++e) {
         tlo[((size_t)i * 2 + dir) * kTwN + e] = (u32)(x * r32 % p);
@@ -228,6 +227,9 @@ int get_plan(DevState* ds, int lg, const Plan** out) {
   }
   CK(cudaMalloc(&pl.tlo_m, tlo.size() * sizeof(u32)), "alloc plan tables");
   CK(cudaMalloc(&pl.thi, thi.size() * sizeof(uint2)), "alloc plan tables");
+  CK(cudaMalloc(&pl.g, gt.size() * sizeof(uint2)), "alloc plan tables");
+  CK(cudaMemcpy(pl.g, gt.data(), gt.size() * sizeof(uint2), cudaMemcpyHostToDevice),
+     "upload plan tables");
   CK(cudaMemcpy(pl.tlo_m, tlo.data(), tlo.size() * sizeof(u32), cudaMemcpyHostToDevice),
      "upload plan tables");
   CK(cudaMemcpy(pl.thi, thi.data(), thi.size() * sizeof(uint2), cudaMemcpyHostToDevice),
@@ -242,6 +244,7 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   t.stw = ds->stw;
   t.tlo_m = pl->tlo_m;
   t.thi = pl->thi;
+  t.g = pl->g;
   for (int i = 0; i < kNumPrimes; ++i) {
     t.scale[i] = pl->scale[i];
     t.scale_sh[i] = pl->scale_sh[i];
@@ -324,16 +327,17 @@ ConvJob make_job(const Layout& ly, void* ws, int lg, int batch) {
   split_lg(lg, &lgR, &lgC);
   j.lgR = lgR;
   j.lgC = lgC;
-  j.in_stride = (long long)ly.in_stride;
-  j.words = (const u32*)(base + ly.off_words);
   j.buf = (u32*)(base + ly.off_buf);
   j.out_words = (u32*)(base + ly.off_out);
-  j.mw = (long long)ly.mw;  // output words per block (also their stride)
+  j.mw = (long long)ly.mw;
   j.tile_state = (unsigned long long*)(base + ly.off_state);
   j.tile_ctr = (u32*)(base + ly.off_ctr);
   j.tiles = (int)ly.tiles;
+  j.maskA = j.maskX = j.maskD = 0xFFFFFFFFu;
   return j;
 }
+
+bool aligned4(const void* p) { return ((uintptr_t)p & 3) == 0; }
 
 }  // namespace
 
@@ -390,29 +394,53 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   while (chunk > 0 && layout_for(g.K, g.lg, g.K, g.mw, chunk).total > workspace_bytes) chunk /= 2;
   if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
   const int msf = byte_order == PAB_ORDER_MSF;
+  // LSF blocks whose words can be read in place (the common case): no pack kernel
+  const bool direct_in = !msf && nbytes % 4 == 0 && in_stride % 4 == 0 && aligned4(x) &&
+                         aligned4(c) && aligned4(d);
+  const bool direct_out = !msf && out_stride % 4 == 0 && aligned4(out);
+  const u32 mask = (n_bits & 31) ? ((1u << (n_bits & 31)) - 1u) : 0xFFFFFFFFu;
   for (u64 b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = (int)((batch - b0) < chunk ? (batch - b0) : chunk);
     const Layout ly = layout_for(g.K, g.lg, g.K, g.mw, nb);
     ConvJob job = make_job(ly, workspace, g.lg, nb);
     job.kA = job.kX = job.kD = (long long)g.K;
+    job.maskA = job.maskX = job.maskD = mask;
     job.nT = (long long)g.K;
     job.nRes = (long long)g.K;
     job.n_mod_bits = (long long)n_bits;
     job.shift = (long long)(n_bits - r_bits);
     job.mw = (long long)g.mw;
     CK(cudaMemsetAsync((char*)workspace + ly.off_state, 0, ly.total - ly.off_state, st), "memset");
-    u32* words = (u32*)((char*)workspace + ly.off_words);
-    const long long wst = 3 * (long long)ly.in_stride;
-    launch_pack(c + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words, wst,
-                (long long)g.K, st);
-    launch_pack(x + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
-                words + ly.in_stride, wst, (long long)g.K, st);
-    launch_pack(d + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
-                words + 2 * ly.in_stride, wst, (long long)g.K, st);
+    if (direct_in) {
+      job.srcA = (const u32*)(c + b0 * in_stride);
+      job.srcX = (const u32*)(x + b0 * in_stride);
+      job.srcD = (const u32*)(d + b0 * in_stride);
+      job.src_stride = (long long)(in_stride / 4);
+    } else {
+      u32* words = (u32*)((char*)workspace + ly.off_words);
+      const long long ws = (long long)ly.in_stride;
+      launch_pack(c + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words,
+                  3 * ws, (long long)g.K, st);
+      launch_pack(x + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words + ws,
+                  3 * ws, (long long)g.K, st);
+      launch_pack(d + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
+                  words + 2 * ws, 3 * ws, (long long)g.K, st);
+      job.srcA = words;
+      job.srcX = words + ws;
+      job.srcD = words + 2 * ws;
+      job.src_stride = 3 * ws;
+    }
+    if (direct_out) {
+      job.out_words = nullptr;
+      job.out_bytes = out + b0 * out_stride;
+      job.out_stride = (long long)out_stride;
+      job.rbytes = (long long)rbytes;
+    }
     launch_conv(job, tab, st);
     launch_carry(job, st);
-    launch_unpack(job.out_words, job.mw, (long long)r_bits, msf, nb, out + b0 * out_stride,
-                  (long long)out_stride, st);
+    if (!direct_out)
+      launch_unpack(job.out_words, job.mw, (long long)r_bits, msf, nb, out + b0 * out_stride,
+                    (long long)out_stride, st);
     CK(cudaGetLastError(), "kernel launch");
   }
   return PAB_OK;
@@ -519,6 +547,10 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
   launch_pack(a, (long long)a_bytes, 8ll * (long long)a_bytes, 0, 1, words, 0, (long long)ka, st);
   launch_pack(b, (long long)b_bytes, 8ll * (long long)b_bytes, 0, 1, words + ly.in_stride, 0,
               (long long)kb, st);
+  job.srcA = words;
+  job.srcX = words + ly.in_stride;
+  job.srcD = nullptr;
+  job.src_stride = 0;
   launch_conv(job, tables_of(ds, pl), st);
   launch_carry(job, st);
   launch_unpack(job.out_words, job.mw, 8ll * (long long)(a_bytes + b_bytes), 0, 1, out,

@@ -3,20 +3,24 @@
 // Pipeline per block (reference path: compress -> fused_mul_add -> mul ->
 // ssa_multiply -> mod_pow2 -> shift_right, pkg/src/modpa/pa.py:175-190,
 // pkg/src/modpa/bignum.py:161-238, pkg/src/modpa/ntt.py:270-284):
-//   k_pack      bytes -> 32-bit words (import_block/split, pa.py:111-125, ntt.py:111-120)
-//   k_col_fwd   column DIF pass of the four-step NTT (forward_ntt, ntt.py:209-212)
-//   k_row       row twiddle + DIF, pointwise product, DIT + twiddle (pointwise_mul, ntt.py:225-243)
-//   k_col_inv   column DIT pass + 1/L scale -> residues mod p_i (inverse_ntt, ntt.py:215-222)
-//   k_carry     CRT + overlap-add + "+d" + carry-lookahead scan + mod 2^n + >> (n-r)
-//               (combine_and_carry ntt.py:246-267, fused_mul_add bignum.py:238,
-//                mod_pow2 bignum.py:161-165, shift_right bignum.py:168-172)
-//   k_unpack    words -> ceil(r/8) bytes (export_block, pa.py:128-132)
-#include "pa_kernels.cuh"
-#include "ntt_panel.cuh"
-
+//   k_col_fwd  column DIF pass of the four-step NTT, reading the operands'
+//              32-bit words straight from the serialized blocks (import_block /
+//              split, pa.py:111-125, ntt.py:111-120; forward_ntt ntt.py:209-212)
+//   k_row      row pass: four-step twiddle, DIF of c and x, pointwise product,
+//              DIT, inverse twiddle (pointwise_mul, ntt.py:225-243)
+//   k_col_inv  column DIT pass + 1/L scale -> residues mod p_i (inverse_ntt, ntt.py:215-222)
+//   k_carry    CRT + overlap-add + "+d" + carry-lookahead scan + mod 2^n + >> (n-r),
+//              writing the key bytes (combine_and_carry ntt.py:246-267, fused_mul_add
+//              bignum.py:238, mod_pow2 bignum.py:161-165, shift_right bignum.py:168-172,
+//              export_block pa.py:128-132)
+//   k_pack / k_unpack  only for MSF or unaligned layouts.
+// For L <= 4096 a single k_row CTA per (block, prime) does the whole transform.
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include "ntt_core.cuh"
+#include "pa_kernels.cuh"
 
 namespace pab {
 
@@ -107,7 +111,7 @@ __device__ __forceinline__ int brev(int x, int bits) {
 }
 
 // ---------------------------------------------------------------------------
-// pack / unpack
+// pack / unpack (MSF byte order or unaligned blocks only)
 
 __global__ void k_pack(const uint8_t* __restrict__ in, long long in_stride, long long n_bits,
                        int msf, u32* __restrict__ words, long long word_stride, long long kw) {
@@ -116,22 +120,17 @@ __global__ void k_pack(const uint8_t* __restrict__ in, long long in_stride, long
   u32* dst = words + (long long)b * word_stride;
   const long long nbytes = (n_bits + 7) >> 3;
   const long long kn = (n_bits + 31) >> 5;
-  const bool aligned = !msf && ((reinterpret_cast<uintptr_t>(src) & 3) == 0);
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < kw;
        j += (long long)gridDim.x * blockDim.x) {
     u32 w = 0;
     if (j < kn) {
       const long long q0 = 4 * j;
-      if (aligned && q0 + 4 <= nbytes) {
-        w = reinterpret_cast<const u32*>(src)[j];
-      } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const long long bi = q0 + q;
-          if (bi < nbytes) {
-            const u32 byte = msf ? src[nbytes - 1 - bi] : src[bi];
-            w |= byte << (8 * q);
-          }
+      for (int q = 0; q < 4; ++q) {
+        const long long bi = q0 + q;
+        if (bi < nbytes) {
+          const u32 byte = msf ? src[nbytes - 1 - bi] : src[bi];
+          w |= byte << (8 * q);
         }
       }
       if (j == kn - 1 && (n_bits & 31)) w &= (1u << (n_bits & 31)) - 1u;
@@ -177,151 +176,401 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
 }
 
 // ---------------------------------------------------------------------------
-// four-step twiddle w_L^(e) in Montgomery form, e < L.
-__device__ __forceinline__ u32 fourstep_tw(const PlanTables& tab, int prime, int dir, u32 e,
-                                           u32 p) {
-  const int off = (prime * 2 + dir) * kTwN;
+// operand word fetch: zero beyond the valid words, mask the last one
+__device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long gi, long long kv,
+                                          u32 mask) {
+  if (gi >= kv) return 0u;
+  const u32 w = __ldg(src + gi);
+  return gi == kv - 1 ? (w & mask) : w;
+}
+
+// four-step twiddle seed w_L^e * 2^32 (Montgomery form, lazy [0, 2p)), e < L
+template <int P>
+__device__ __forceinline__ u32 tw_seed(const PlanTables& tab, int dir, u32 e) {
+  const int off = (P * 2 + dir) * kTwN;
   const u32 lo = __ldg(&tab.tlo_m[off + (e & (kTwN - 1))]);
   const uint2 hi = __ldg(&tab.thi[off + (e >> kTwLg)]);
-  return shoup(lo, hi, p);
+  return shoup(lo, hi, PK<P>::p);
 }
 
 // ---------------------------------------------------------------------------
-// Column pass (forward): CT columns x R rows per CTA; DIF over rows.
-// grid: x = C / CT, y = prime, z = b * 2 + op.
-__global__ void k_col_fwd(ConvJob job, PlanTables tab, int lct) {
+// Row pass.  CTA: NR = 2^lnr rows of one (block, prime); smem holds the NR
+// c-rows (A) then the NR x-rows (X), each sm_len(LGC) words.
+// SMALL (lgR == 0): the row is the whole transform; read the operand words,
+// write scaled residues.
+template <int P, int LGC, bool SMALL>
+__device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& tab, int lnr) {
   extern __shared__ u32 smem[];
-  const int prime = blockIdx.y;
-  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
-  const PrimeInfo pi = c_primes[prime];
-  const int lgR = job.lgR, lgC = job.lgC;
-  const int CT = 1 << lct;
-  const long long L = 1ll << job.lg;
-  const int c0 = blockIdx.x << lct;
-  const u32* src = job.words + ((long long)b * 3 + op) * job.in_stride;
-  const long long kvalid = op == 0 ? job.kA : job.kX;
-  const int total = (1 << lgR) << lct;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx >> lct, t = idx & (CT - 1);
-    const long long gi = ((long long)r << lgC) + c0 + t;
-    const u32 raw = gi < kvalid ? __ldg(&src[gi]) : 0u;
-    smem[pidx(r, t, lct)] = shoup(raw, 1u, pi.one_sh, pi.p);
-  }
-  __syncthreads();
-  const uint2* tw = tab.stw + (prime * 2 + 0) * kTwN;
-  panel_dif<false>(smem, lgR, lct, lct, 1, 0, tw, pi.p, pi.two_p);
-  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + prime) * L;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx >> lct, t = idx & (CT - 1);
-    dst[((long long)r << lgC) + c0 + t] = smem[pidx(r, t, lct)];
-  }
-}
-
-// Column pass (inverse): DIT over rows, scale, full reduction, residues -> slot A.
-__global__ void k_col_inv(ConvJob job, PlanTables tab, int lct) {
-  extern __shared__ u32 smem[];
-  const int prime = blockIdx.y;
-  const int b = blockIdx.z;
-  const PrimeInfo pi = c_primes[prime];
-  const int lgR = job.lgR, lgC = job.lgC;
-  const int CT = 1 << lct;
-  const long long L = 1ll << job.lg;
-  const int c0 = blockIdx.x << lct;
-  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + prime) * L;
-  const int total = (1 << lgR) << lct;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx >> lct, t = idx & (CT - 1);
-    smem[pidx(r, t, lct)] = src[((long long)r << lgC) + c0 + t];
-  }
-  __syncthreads();
-  const uint2* tw = tab.stw + (prime * 2 + 1) * kTwN;
-  panel_dit<false>(smem, lgR, lct, lct, 1, 0, tw, pi.p, pi.two_p);
-  u32* dst = job.buf + (((long long)b * 2 + 0) * 3 + prime) * L;
-  const u32 sc = tab.scale[prime], sc_sh = tab.scale_sh[prime];
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx >> lct, t = idx & (CT - 1);
-    const long long gi = ((long long)r << lgC) + c0 + t;
-    if (gi < job.nRes) dst[gi] = red(shoup(smem[pidx(r, t, lct)], sc, sc_sh, pi.p), pi.p);
-  }
-}
-
-// Row pass: NR rows per CTA, A and X interleaved (t = 2*row + op).
-// Forward four-step twiddle, DIF (A and X), pointwise Montgomery product,
-// DIT (X), inverse twiddle; R == 1 is the whole transform (small blocks):
-// inputs come straight from the packed words and residues are written out.
-// grid: x = R / NR, y = prime, z = b.
-__global__ void k_row(ConvJob job, PlanTables tab, int lnr) {
-  extern __shared__ u32 smem[];
-  const int prime = blockIdx.y;
-  const int b = blockIdx.z;
-  const PrimeInfo pi = c_primes[prime];
-  const int lgR = job.lgR, lgC = job.lgC;
-  const int C = 1 << lgC;
+  constexpr PassPlan PP = pass_plan(LGC);
+  constexpr int T = sm_len(LGC);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int NR = 1 << lnr;
-  const int lnc = lnr + 1;
-  const long long L = 1ll << job.lg;
+  const int b = blockIdx.z;
   const int q0 = blockIdx.x << lnr;
-  const bool single = (lgR == 0);
-  const int total = (2 * NR) << lgC;
+  const int lgR = job.lgR;
+  const long long L = 1ll << job.lg;
+  u32* sA = smem;
+  u32* sX = smem + NR * T;
+  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
+  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
+  u32* gA = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;  // also the residue slot
+  u32* gX = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
+  const u32* wA = job.srcA + (long long)b * job.src_stride;
+  const u32* wX = job.srcX + (long long)b * job.src_stride;
 
-  // load
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int i = idx & (C - 1);
-    const int t = idx >> lgC;
-    const int row = t >> 1, op = t & 1;
-    u32 v;
-    if (single) {
-      const u32* src = job.words + ((long long)b * 3 + op) * job.in_stride;
-      const long long kvalid = op == 0 ? job.kA : job.kX;
-      const u32 raw = i < kvalid ? __ldg(&src[i]) : 0u;
-      v = shoup(raw, 1u, pi.one_sh, pi.p);
-    } else {
-      const u32* src = job.buf + (((long long)b * 2 + op) * 3 + prime) * L;
-      v = src[((long long)(q0 + row) << lgC) + i];
-      // forward four-step twiddle w_L^(i * k1), k1 = bitrev_R(q)
-      const u32 k1 = (u32)brev(q0 + row, lgR);
-      const u32 m = fourstep_tw(tab, prime, 0, (u32)i * k1, pi.p);
-      v = montmul(v, m, pi.p, pi.p_mont);
-    }
-    smem[tidx(i, t, lgC)] = v;
-  }
-  __syncthreads();
-  const uint2* twf = tab.stw + (prime * 2 + 0) * kTwN;
-  const uint2* twi = tab.stw + (prime * 2 + 1) * kTwN;
-  panel_dif<true>(smem, lgC, lnc, 0, 1, 0, twf, pi.p, pi.two_p);
-  // pointwise product into the X slot (factor 2^-32 folded into the final scale)
-  for (int idx = threadIdx.x; idx < (NR << lgC); idx += blockDim.x) {
-    const int i = idx & (C - 1);
-    const int row = idx >> lgC;
-    const int ia = tidx(i, 2 * row, lgC), ix = tidx(i, 2 * row + 1, lgC);
-    smem[ix] = montmul(smem[ia], smem[ix], pi.p, pi.p_mont);
-  }
-  __syncthreads();
-  panel_dit<true>(smem, lgC, lnr, 0, 2, 1, twi, pi.p, pi.two_p);
-  // store
-  for (int idx = threadIdx.x; idx < (NR << lgC); idx += blockDim.x) {
-    const int i = idx & (C - 1);
-    const int row = idx >> lgC;
-    u32 v = smem[tidx(i, 2 * row + 1, lgC)];
-    if (single) {
-      if (i < job.nRes) {
-        u32* dst = job.buf + (((long long)b * 2 + 0) * 3 + prime) * L;
-        dst[i] = red(shoup(v, tab.scale[prime], tab.scale_sh[prime], pi.p), pi.p);
+  // ---- pass 0: global -> (twiddle) -> DIF top stages -> smem (A and X share twiddles)
+  if constexpr (PP.n > 1) {
+    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
+      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
+      const int q = q0 + row;
+      u32 v[2][1 << RS0];
+      if constexpr (SMALL) {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const long long gi = o + (k << SLO0);
+          v[0][k] = shoup(fetch_word(wA, gi, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
+          v[1][k] = shoup(fetch_word(wX, gi, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+        }
+      } else {
+        const u32* ra = gA + ((long long)q << LGC) + o;
+        const u32* rx = gX + ((long long)q << LGC) + o;
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          v[0][k] = ra[k << SLO0];
+          v[1][k] = rx[k << SLO0];
+        }
+        const u32 k1 = (u32)brev(q, lgR);
+        u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
+        const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          v[0][k] = mont<P>(v[0][k], m);
+          v[1][k] = mont<P>(v[1][k], m);
+          m = shoup(m, gam, PK<P>::p);
+        }
       }
-    } else {
-      const u32 k1 = (u32)brev(q0 + row, lgR);
-      const u32 m = fourstep_tw(tab, prime, 1, (u32)i * k1, pi.p);
-      v = montmul(red(v, pi.two_p), m, pi.p, pi.p_mont);
-      u32* dst = job.buf + (((long long)b * 2 + 1) * 3 + prime) * L;
-      dst[((long long)(q0 + row) << lgC) + i] = v;
+      dif_rt<P, RS0, SLO0, 2>(v, twf + o);
+      const int base = row * T + sm_idx(o);
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        sA[base + k * sm_step(SLO0)] = v[0][k];
+        sX[base + k * sm_step(SLO0)] = v[1][k];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- pass 1 (middle), forward, A and X
+  if constexpr (PP.n == 3) {
+    constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+    constexpr int LGG = LGC - RS1;  // groups per row (log2)
+    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+      const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+      const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
+      u32 v[2][1 << RS1];
+#pragma unroll
+      for (int k = 0; k < (1 << RS1); ++k) {
+        v[0][k] = sA[base + k * sm_step(SLO1)];
+        v[1][k] = sX[base + k * sm_step(SLO1)];
+      }
+      dif_rt<P, RS1, SLO1, 2>(v, twf + o);
+#pragma unroll
+      for (int k = 0; k < (1 << RS1); ++k) {
+        sA[base + k * sm_step(SLO1)] = v[0][k];
+        sX[base + k * sm_step(SLO1)] = v[1][k];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- last DIF pass (lowest stages) + pointwise + first DIT pass
+  constexpr int RSL = PP.rs[PP.n - 1];
+  {
+    constexpr int LGG = LGC - RSL;
+    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+      u32 a[1][1 << RSL], x[1][1 << RSL];
+      int base = 0;
+      if constexpr (PP.n == 1) {  // whole transform in registers, straight from global
+        const int q = q0 + row;
+        if constexpr (SMALL) {
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            a[0][k] = shoup(fetch_word(wA, k, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
+            x[0][k] = shoup(fetch_word(wX, k, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+          }
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 0, 0u);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            a[0][k] = mont<P>(gA[((long long)q << LGC) + k], m);
+            x[0][k] = mont<P>(gX[((long long)q << LGC) + k], m);
+            m = shoup(m, gam, PK<P>::p);
+          }
+        }
+      } else {
+        base = row * T + sm_idx(g << RSL);
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) a[0][k] = sA[base + k];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = sX[base + k];
+      }
+      dif_ct<P, RSL, 1>(a);
+      dif_ct<P, RSL, 1>(x);
+#pragma unroll
+      for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
+      dit_ct<P, RSL>(x[0]);
+      if constexpr (PP.n == 1) {
+        const int q = q0 + row;
+        if constexpr (SMALL) {
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k)
+            if (k < job.nRes)
+              gA[k] = red(shoup(x[0][k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 1, 0u);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            gX[((long long)q << LGC) + k] = mont<P>(red(x[0][k], PK<P>::two_p), m);
+            m = shoup(m, gam, PK<P>::p);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) sX[base + k] = x[0][k];
+      }
+    }
+  }
+  if constexpr (PP.n > 1) {
+    __syncthreads();
+    // ---- pass 1 inverse (X)
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      constexpr int LGG = LGC - RS1;
+      for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+        const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
+        u32 v[1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[k] = sX[base + k * sm_step(SLO1)];
+        dit_rt<P, RS1, SLO1>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) sX[base + k * sm_step(SLO1)] = v[k];
+      }
+      __syncthreads();
+    }
+    // ---- pass 0 inverse (X) -> inverse twiddle -> global (or scaled residues)
+    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
+      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
+      const int q = q0 + row;
+      const int base = row * T + sm_idx(o);
+      u32 v[1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) v[k] = sX[base + k * sm_step(SLO0)];
+      dit_rt<P, RS0, SLO0>(v, twi + o);
+      if constexpr (SMALL) {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const long long gi = o + (k << SLO0);
+          if (gi < job.nRes)
+            gA[gi] = red(shoup(v[k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
+        }
+      } else {
+        const u32 k1 = (u32)brev(q, lgR);
+        u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
+        const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+        u32* rx = gX + ((long long)q << LGC) + o;
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
+          m = shoup(m, gam, PK<P>::p);
+        }
+      }
     }
   }
 }
 
+template <int LGC, bool SMALL>
+__global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
+  switch (blockIdx.y) {
+    case 0: row_body<0, LGC, SMALL>(job, tab, lnr); break;
+    case 1: row_body<1, LGC, SMALL>(job, tab, lnr); break;
+    default: row_body<2, LGC, SMALL>(job, tab, lnr); break;
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Carry: CRT of the three residues, overlap-add of 96-bit coefficients at
+// Column passes.  CTA: CT = 2^lct adjacent columns x R rows, interleaved in
+// smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
+// broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
+// scaled residues.
+template <int P, int LGR>
+__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int CT = 1 << lct;
+  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
+  const int lgC = job.lgC;
+  const long long L = 1ll << job.lg;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
+  const long long kv = op ? job.kX : job.kA;
+  const u32 mask = op ? job.maskX : job.maskA;
+  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
+  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
+
+  if constexpr (PP.n == 1) {
+    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
+      u32 v[1][1 << LGR];
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k)
+        v[0][k] = shoup(fetch_word(src, ((long long)k << lgC) + c0 + t, kv, mask), 1u,
+                        PK<P>::one_sh, PK<P>::p);
+      dif_ct<P, LGR, 1>(v);
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) dst[((long long)k << lgC) + c0 + t] = v[0][k];
+    }
+  } else {
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      u32 v[1][1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        const long long gi = ((long long)(o + (k << SLO0)) << lgC) + c0 + t;
+        v[0][k] = shoup(fetch_word(src, gi, kv, mask), 1u, PK<P>::one_sh, PK<P>::p);
+      }
+      dif_rt<P, RS0, SLO0, 1>(v, twf + o);
+      const int base = sm_idx(o) * CT + t;
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) smem[base + k * sm_step(SLO0) * CT] = v[0][k];
+    }
+    __syncthreads();
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
+        const int t = task & (CT - 1), g = task >> lct;
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
+        u32 v[1][1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[0][k] = smem[base + k * sm_step(SLO1) * CT];
+        dif_rt<P, RS1, SLO1, 1>(v, twf + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[0][k];
+      }
+      __syncthreads();
+    }
+    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
+      const int t = task & (CT - 1), g = task >> lct;
+      const int base = (33 * g) * CT + t;
+      u32 v[1][32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[0][k] = smem[base + k * CT];
+      dif_ct<P, 5, 1>(v);
+      u32* d = dst + ((long long)(g << 5) << lgC) + c0 + t;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[(long long)k << lgC] = v[0][k];
+    }
+  }
+}
+
+template <int P, int LGR>
+__device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int CT = 1 << lct;
+  const int b = blockIdx.z;
+  const int lgC = job.lgC;
+  const long long L = 1ll << job.lg;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
+  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
+  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
+  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
+
+  if constexpr (PP.n == 1) {
+    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
+      u32 v[1 << LGR];
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) v[k] = src[((long long)k << lgC) + c0 + t];
+      dit_ct<P, LGR>(v);
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) {
+        const long long gi = ((long long)k << lgC) + c0 + t;
+        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+      }
+    }
+  } else {
+    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
+      const int t = task & (CT - 1), g = task >> lct;
+      const u32* s = src + ((long long)(g << 5) << lgC) + c0 + t;
+      u32 v[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = s[(long long)k << lgC];
+      dit_ct<P, 5>(v);
+      const int base = (33 * g) * CT + t;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) smem[base + k * CT] = v[k];
+    }
+    __syncthreads();
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
+        const int t = task & (CT - 1), g = task >> lct;
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
+        u32 v[1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[k] = smem[base + k * sm_step(SLO1) * CT];
+        dit_rt<P, RS1, SLO1>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[k];
+      }
+      __syncthreads();
+    }
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      const int base = sm_idx(o) * CT + t;
+      u32 v[1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) v[k] = smem[base + k * sm_step(SLO0) * CT];
+      dit_rt<P, RS0, SLO0>(v, twi + o);
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        const long long gi = ((long long)(o + (k << SLO0)) << lgC) + c0 + t;
+        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+      }
+    }
+  }
+}
+
+template <int LGR>
+__global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: col_fwd_body<0, LGR>(job, tab, lct); break;
+    case 1: col_fwd_body<1, LGR>(job, tab, lct); break;
+    default: col_fwd_body<2, LGR>(job, tab, lct); break;
+  }
+}
+template <int LGR>
+__global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: col_inv_body<0, LGR>(job, tab, lct); break;
+    case 1: col_inv_body<1, LGR>(job, tab, lct); break;
+    default: col_inv_body<2, LGR>(job, tab, lct); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Carry: CRT of the three residues, overlap-add of the 96-bit coefficients at
 // 32-bit stride, + D, carry-lookahead scan (decoupled look-back across tiles),
-// mask to n_mod_bits, shift right, write output words.
+// mask to n_mod_bits, shift right, write the key.
 
 struct CarryFn {  // c -> q + (c >= t); id marks the identity
   u32 q, t;
@@ -345,16 +594,16 @@ __device__ __forceinline__ u32 cf_apply(CarryFn f, u32 c) {
 __device__ __forceinline__ void crt3(u32 r0, u32 r1, u32 r2, u32& w0, u32& w1, u32& w2) {
   const CrtConst& k = c_crt;
   const u32 v0 = r0;
-  u32 x1 = r1 + 2u * k.p1 - v0;
-  u32 v1 = red(shoup(x1, k.inv01, k.inv01_sh, k.p1), k.p1);
+  const u32 x1 = r1 + 2u * k.p1 - v0;
+  const u32 v1 = red(shoup(x1, k.inv01, k.inv01_sh, k.p1), k.p1);
   u32 u = v0 + shoup(v1, k.p0m2, k.p0m2_sh, k.p2);  // [0, 4 p2)
   u = red(u, 2u * k.p2);
-  u32 x2 = r2 + 2u * k.p2 - u;
-  u32 v2 = red(shoup(x2, k.inv012, k.inv012_sh, k.p2), k.p2);
-  u64 lo = (u64)v0 + (u64)k.p0 * v1;        // < 2^61
-  u64 prod_lo = k.p0p1 * (u64)v2;
+  const u32 x2 = r2 + 2u * k.p2 - u;
+  const u32 v2 = red(shoup(x2, k.inv012, k.inv012_sh, k.p2), k.p2);
+  const u64 lo = (u64)v0 + (u64)k.p0 * v1;  // < 2^61
+  const u64 prod_lo = k.p0p1 * (u64)v2;
   u64 prod_hi = __umul64hi(k.p0p1, (u64)v2);
-  u64 s = lo + prod_lo;
+  const u64 s = lo + prod_lo;
   prod_hi += (s < lo) ? 1ull : 0ull;
   w0 = (u32)s;
   w1 = (u32)(s >> 32);
@@ -373,7 +622,7 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry(ConvJob job) {
   const u32* res0 = job.buf + (((long long)b * 2 + 0) * 3 + 0) * L;
   const u32* res1 = res0 + L;
   const u32* res2 = res1 + L;
-  const u32* dw = job.words + ((long long)b * 3 + 2) * job.in_stride;
+  const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
   const long long w0 = (long long)tile * kCarryTile + (long long)threadIdx.x * kCarryItems;
 
   // column sums S[j] for words w0 .. w0+8
@@ -392,7 +641,7 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry(ConvJob job) {
 #pragma unroll
     for (int j = 0; j <= kCarryItems; ++j) {
       const long long w = w0 + j;
-      const u32 d = (w < job.kD) ? __ldg(&dw[w]) : 0u;
+      const u32 d = dw ? fetch_word(dw, w, job.kD, job.maskD) : 0u;
       S[j] = (u64)A0[j + 2] + A1[j + 1] + A2[j] + d;
     }
   }
@@ -493,17 +742,55 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry(ConvJob job) {
   // output words y_j = T >> shift
   const long long ws = job.shift >> 5;
   const int sh = (int)(job.shift & 31);
-  u32* out = job.out_words + (long long)b * job.mw;
+  if (job.out_words) {
+    u32* out = job.out_words + (long long)b * job.mw;
 #pragma unroll
-  for (int j = 0; j < kCarryItems; ++j) {
-    const long long oj = w0 + j - ws;
-    if (oj >= 0 && oj < job.mw) {
-      out[oj] = sh ? ((T[j] >> sh) | (T[j + 1] << (32 - sh))) : T[j];
+    for (int j = 0; j < kCarryItems; ++j) {
+      const long long oj = w0 + j - ws;
+      if (oj >= 0 && oj < job.mw) out[oj] = sh ? ((T[j] >> sh) | (T[j + 1] << (32 - sh))) : T[j];
+    }
+  } else {  // LSF bytes, word-aligned block starts
+    uint8_t* out = job.out_bytes + (long long)b * job.out_stride;
+#pragma unroll
+    for (int j = 0; j < kCarryItems; ++j) {
+      const long long oj = w0 + j - ws;
+      if (oj >= 0 && oj < job.mw) {
+        const u32 y = sh ? ((T[j] >> sh) | (T[j + 1] << (32 - sh))) : T[j];
+        if (4 * oj + 4 <= job.rbytes) {
+          reinterpret_cast<u32*>(out)[oj] = y;
+        } else {
+          for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q)
+            out[4 * oj + q] = (uint8_t)(y >> (8 * q));
+        }
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
+// dispatch over compile-time transform sizes
+
+typedef void (*ConvKernel)(ConvJob, PlanTables, int);
+
+static ConvKernel row_kernel(int lg, bool small) {
+  switch (lg) {
+#define PAB_ROW(L) \
+  case L: return small ? k_row<L, true> : k_row<L, false>;
+    PAB_ROW(1) PAB_ROW(2) PAB_ROW(3) PAB_ROW(4) PAB_ROW(5) PAB_ROW(6) PAB_ROW(7) PAB_ROW(8)
+    PAB_ROW(9) PAB_ROW(10) PAB_ROW(11) PAB_ROW(12)
+#undef PAB_ROW
+    default: return nullptr;
+  }
+}
+static ConvKernel col_kernel(int lg, bool inv) {
+  switch (lg) {
+#define PAB_COL(L) \
+  case L: return inv ? k_col_inv<L> : k_col_fwd<L>;
+    PAB_COL(6) PAB_COL(7) PAB_COL(8) PAB_COL(9) PAB_COL(10) PAB_COL(11) PAB_COL(12)
+#undef PAB_COL
+    default: return nullptr;
+  }
+}
 
 static int col_lct(int lgR, int lgC) {
   int lct = 14 - lgR;  // ~16K words per CTA
@@ -516,31 +803,31 @@ static int col_lct(int lgR, int lgC) {
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
   if (job.lgR == 0) {
-    const int lnr = 0;
-    const size_t sm = (size_t)tm_stride(job.lgC) * (2 << lnr) * 4;
+    const size_t sm = (size_t)sm_len(job.lgC) * 2 * 4;
     prof::Scope ps_("k_row_single", st);
-    k_row<<<dim3(1, kNumPrimes, job.batch), threads, sm, st>>>(job, tab, lnr);
+    row_kernel(job.lgC, true)<<<dim3(1, kNumPrimes, job.batch), threads, sm, st>>>(job, tab, 0);
     return;
   }
   const int lct = col_lct(job.lgR, job.lgC);
-  const size_t smc = (size_t)panel_words(job.lgR, lct) * 4;
+  const size_t smc = (size_t)sm_len(job.lgR) * (1u << lct) * 4;
   {
     prof::Scope ps_("k_col_fwd", st);
-    k_col_fwd<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(
-        job, tab, lct);
+    col_kernel(job.lgR, false)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads,
+                                 smc, st>>>(job, tab, lct);
   }
-  int lnr = 13 - job.lgC;  // ~8K words (A+X) per CTA
+  int lnr = 13 - job.lgC;  // 8K words of rows (A+X: 16K words) per CTA
   if (lnr < 0) lnr = 0;
   if (lnr > job.lgR) lnr = job.lgR;
-  const size_t smr = (size_t)tm_stride(job.lgC) * (2 << lnr) * 4;
+  const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    k_row<<<dim3(1u << (job.lgR - lnr), kNumPrimes, job.batch), threads, smr, st>>>(job, tab, lnr);
+    row_kernel(job.lgC, false)<<<dim3(1u << (job.lgR - lnr), kNumPrimes, job.batch), threads, smr,
+                                 st>>>(job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    k_col_inv<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc, st>>>(job, tab,
-                                                                                        lct);
+    col_kernel(job.lgR, true)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc,
+                                st>>>(job, tab, lct);
   }
 }
 
@@ -549,11 +836,16 @@ void launch_carry(const ConvJob& job, cudaStream_t st) {
   k_carry<<<dim3(job.tiles, job.batch), kCarryThreads, 0, st>>>(job);
 }
 
-// Opt every dynamic-smem kernel into > 48 KB once.
+// Opt every dynamic-smem kernel into > 48 KB once per device.
 void set_kernel_attrs() {
-  cudaFuncSetAttribute(k_col_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_col_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int lg = 1; lg <= 12; ++lg) {
+    for (int s = 0; s < 2; ++s) {
+      ConvKernel k = row_kernel(lg, s != 0);
+      if (k) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      ConvKernel c = col_kernel(lg, s != 0);
+      if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
+  }
 }
 
 }  // namespace pab

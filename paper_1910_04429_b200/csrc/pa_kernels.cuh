@@ -7,13 +7,14 @@
 namespace pab {
 
 // Device twiddle tables for one plan (one transform length L = 2^lg).
-// All arrays are [prime][dir] with dir 0 = forward (w), 1 = inverse (w^-1).
+// All arrays are [prime][dir][4096] with dir 0 = forward (w), 1 = inverse (w^-1).
 struct PlanTables {
-  const uint2* stw;    // [3][2][4096] stage twiddles tw[h+e] = w_{2h}^e, Shoup pairs
-  const u32* tlo_m;    // [3][2][4096] Montgomery form of w_L^e, e < 4096
-  const uint2* thi;    // [3][2][4096] Shoup pairs of w_L^(4096 j)
-  u32 scale[3];        // L^-1 * 2^32 mod p (undoes the transform length and the
-  u32 scale_sh[3];     // Montgomery factor of the pointwise product), Shoup pair
+  const uint2* stw;    // stage twiddles tw[h+e] = w_{2h}^e (Shoup pairs), h <= 2048
+  const u32* tlo_m;    // Montgomery form of w_L^e, e < 4096
+  const uint2* thi;    // Shoup pairs of w_L^(4096 j)
+  const uint2* g;      // Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row-pass twiddle step)
+  u32 scale[3];        // L^-1 * 2^32 mod p: undoes the length and the Montgomery factor
+  u32 scale_sh[3];     // of the pointwise product (Shoup companions)
 };
 
 struct CrtConst {
@@ -25,20 +26,27 @@ struct CrtConst {
 };
 
 // One convolution-product job over a batch of independent blocks:
-//   T = (A * X + D) mod 2^n_mod_bits (as words), out = T >> shift (mw words).
+//   T = (A * X + D) mod 2^n_mod_bits (as 32-bit words), out = T >> shift.
 struct ConvJob {
   int batch;
-  int lg, lgR, lgC;            // L = 2^lg = R * C (R = 1: single-pass path)
-  long long kA, kX, kD;        // valid input words per block (A, X, D)
-  long long in_stride;         // words between consecutive blocks' operand slots
-  const u32* words;            // [batch][3][in_stride]: slot 0 = A, 1 = X, 2 = D
-  u32* buf;                    // [batch][2][3][L] transform buffers
+  int lg, lgR, lgC;            // L = 2^lg = R * C (R = 1: single-CTA path)
+  // operands as little-endian 32-bit words; block b at src + b * src_stride
+  const u32* srcA;
+  const u32* srcX;
+  const u32* srcD;             // may be null (no addend)
+  long long src_stride;        // in words
+  long long kA, kX, kD;        // valid words per block
+  u32 maskA, maskX, maskD;     // applied to the last valid word (bits >= n)
+  u32* buf;                    // [batch][2][3][L] transform buffers (slot A reused for residues)
   long long nT;                // T words computed
   long long nRes;              // residues stored (min(nT, L))
   long long n_mod_bits;        // T is reduced mod 2^n_mod_bits
   long long shift;             // output = T >> shift
   long long mw;                // output words per block
-  u32* out_words;              // [batch][mw]
+  u32* out_words;              // [batch][mw], or null: write LSF bytes directly
+  uint8_t* out_bytes;          // block b at out_bytes + b * out_stride, rbytes each
+  long long out_stride;
+  long long rbytes;
   unsigned long long* tile_state;  // [batch][tiles] look-back states (zeroed)
   u32* tile_ctr;               // [batch] tile tickets (zeroed)
   int tiles;                   // carry tiles per block
@@ -49,6 +57,7 @@ constexpr int kCarryItems = 8;
 constexpr int kCarryTile = kCarryThreads * kCarryItems;
 
 void upload_constants(const PrimeInfo* primes, const CrtConst& crt);
+void set_kernel_attrs();
 
 // bytes (LSF or MSF) -> u32 words, zero-padded to kw words, bits >= n cleared.
 void launch_pack(const uint8_t* in, long long in_stride_bytes, long long n_bits, int msf,
@@ -56,8 +65,9 @@ void launch_pack(const uint8_t* in, long long in_stride_bytes, long long n_bits,
 // u32 words -> ceil(m/8) bytes per block (LSF or MSF).
 void launch_unpack(const u32* words, long long word_stride, long long m_bits, int msf, int batch,
                    uint8_t* out, long long out_stride_bytes, cudaStream_t st);
-// transform + pointwise + inverse -> residues in buf slot A; then carry.
+// forward transforms + pointwise + inverse -> residues in buf slot A.
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st);
+// CRT + carry + mask + shift -> output.
 void launch_carry(const ConvJob& job, cudaStream_t st);
 
 }  // namespace pab

@@ -1,0 +1,6 @@
+# dev loop: parity tests then quick perf (library is prebuilt here and shipped)
+set -e
+make -s -C oracle
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -x -q -m gpu ${PYTEST_ARGS:-} 2>&1 | tail -15
+timeout 300 python scripts/quick_perf.py ${QP_ARGS:-}
