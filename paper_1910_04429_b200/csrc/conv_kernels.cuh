@@ -1,0 +1,455 @@
+// Size-specialised NTT conv kernels (instantiated per transform size in
+// conv_lg*.cu so they compile in parallel).  See pa_kernels.cu for the pipeline.
+#pragma once
+#include "ntt_core.cuh"
+#include "pa_kernels.cuh"
+
+namespace pab {
+
+typedef void (*ConvKernel)(ConvJob, PlanTables, int);
+struct ConvKernels {
+  ConvKernel row, row_small, col_fwd, col_inv;
+};
+
+__device__ __forceinline__ int brev(int x, int bits) {
+  return bits == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - bits));
+}
+
+// operand word fetch: zero beyond the valid words, mask the last one
+__device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long gi, long long kv,
+                                          u32 mask) {
+  if (gi >= kv) return 0u;
+  const u32 w = __ldg(src + gi);
+  return gi == kv - 1 ? (w & mask) : w;
+}
+
+// four-step twiddle seed w_L^e * 2^32 (Montgomery form, lazy [0, 2p)), e < L
+template <int P>
+__device__ __forceinline__ u32 tw_seed(const PlanTables& tab, int dir, u32 e) {
+  const int off = (P * 2 + dir) * kTwN;
+  const u32 lo = __ldg(&tab.tlo_m[off + (e & (kTwN - 1))]);
+  const uint2 hi = __ldg(&tab.thi[off + (e >> kTwLg)]);
+  return shoup(lo, hi, PK<P>::p);
+}
+
+// ---------------------------------------------------------------------------
+// Row pass.  CTA: NR = 2^lnr rows of one (block, prime); smem holds the NR
+// c-rows (A) then the NR x-rows (X), each sm_len(LGC) words.
+// SMALL (lgR == 0): the row is the whole transform; read the operand words,
+// write scaled residues.
+template <int P, int LGC, bool SMALL>
+__device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& tab, int lnr) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGC);
+  constexpr int T = sm_len(LGC);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int NR = 1 << lnr;
+  const int b = blockIdx.z;
+  const int q0 = blockIdx.x << lnr;
+  const int lgR = job.lgR;
+  const long long L = 1ll << job.lg;
+  u32* sA = smem;
+  u32* sX = smem + NR * T;
+  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
+  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
+  u32* gA = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;  // also the residue slot
+  u32* gX = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
+  const u32* wA = job.srcA + (long long)b * job.src_stride;
+  const u32* wX = job.srcX + (long long)b * job.src_stride;
+
+  // ---- pass 0: global -> (twiddle) -> DIF top stages -> smem (A and X share twiddles)
+  if constexpr (PP.n > 1) {
+    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
+      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
+      const int q = q0 + row;
+      u32 v[2][1 << RS0];
+      if constexpr (SMALL) {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const long long gi = o + (k << SLO0);
+          v[0][k] = shoup(fetch_word(wA, gi, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
+          v[1][k] = shoup(fetch_word(wX, gi, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+        }
+      } else {
+        const u32* ra = gA + ((long long)q << LGC) + o;
+        const u32* rx = gX + ((long long)q << LGC) + o;
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          v[0][k] = ra[k << SLO0];
+          v[1][k] = rx[k << SLO0];
+        }
+        const u32 k1 = (u32)brev(q, lgR);
+        u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
+        const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          v[0][k] = mont<P>(v[0][k], m);
+          v[1][k] = mont<P>(v[1][k], m);
+          m = shoup(m, gam, PK<P>::p);
+        }
+      }
+      dif_rt<P, RS0, SLO0, 2>(v, twf + o);
+      const int base = row * T + sm_idx(o);
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        sA[base + k * sm_step(SLO0)] = v[0][k];
+        sX[base + k * sm_step(SLO0)] = v[1][k];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- pass 1 (middle), forward, A and X
+  if constexpr (PP.n == 3) {
+    constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+    constexpr int LGG = LGC - RS1;  // groups per row (log2)
+    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+      const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+      const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
+      u32 v[2][1 << RS1];
+#pragma unroll
+      for (int k = 0; k < (1 << RS1); ++k) {
+        v[0][k] = sA[base + k * sm_step(SLO1)];
+        v[1][k] = sX[base + k * sm_step(SLO1)];
+      }
+      dif_rt<P, RS1, SLO1, 2>(v, twf + o);
+#pragma unroll
+      for (int k = 0; k < (1 << RS1); ++k) {
+        sA[base + k * sm_step(SLO1)] = v[0][k];
+        sX[base + k * sm_step(SLO1)] = v[1][k];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- last DIF pass (lowest stages) + pointwise + first DIT pass
+  constexpr int RSL = PP.rs[PP.n - 1];
+  {
+    constexpr int LGG = LGC - RSL;
+    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+      u32 a[1][1 << RSL], x[1][1 << RSL];
+      int base = 0;
+      if constexpr (PP.n == 1) {  // whole transform in registers, straight from global
+        const int q = q0 + row;
+        if constexpr (SMALL) {
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            a[0][k] = shoup(fetch_word(wA, k, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
+            x[0][k] = shoup(fetch_word(wX, k, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+          }
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 0, 0u);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            a[0][k] = mont<P>(gA[((long long)q << LGC) + k], m);
+            x[0][k] = mont<P>(gX[((long long)q << LGC) + k], m);
+            m = shoup(m, gam, PK<P>::p);
+          }
+        }
+      } else {
+        base = row * T + sm_idx(g << RSL);
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) a[0][k] = sA[base + k];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = sX[base + k];
+      }
+      dif_ct<P, RSL, 1>(a);
+      dif_ct<P, RSL, 1>(x);
+#pragma unroll
+      for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
+      dit_ct<P, RSL>(x[0]);
+      if constexpr (PP.n == 1) {
+        const int q = q0 + row;
+        if constexpr (SMALL) {
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k)
+            if (k < job.nRes)
+              gA[k] = red(shoup(x[0][k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 1, 0u);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RSL); ++k) {
+            gX[((long long)q << LGC) + k] = mont<P>(red(x[0][k], PK<P>::two_p), m);
+            m = shoup(m, gam, PK<P>::p);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) sX[base + k] = x[0][k];
+      }
+    }
+  }
+  if constexpr (PP.n > 1) {
+    __syncthreads();
+    // ---- pass 1 inverse (X)
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      constexpr int LGG = LGC - RS1;
+      for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
+        const int row = task >> LGG, g = task & ((1 << LGG) - 1);
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
+        u32 v[1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[k] = sX[base + k * sm_step(SLO1)];
+        dit_rt<P, RS1, SLO1>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) sX[base + k * sm_step(SLO1)] = v[k];
+      }
+      __syncthreads();
+    }
+    // ---- pass 0 inverse (X) -> inverse twiddle -> global (or scaled residues)
+    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
+      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
+      const int q = q0 + row;
+      const int base = row * T + sm_idx(o);
+      u32 v[1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) v[k] = sX[base + k * sm_step(SLO0)];
+      dit_rt<P, RS0, SLO0>(v, twi + o);
+      if constexpr (SMALL) {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const long long gi = o + (k << SLO0);
+          if (gi < job.nRes)
+            gA[gi] = red(shoup(v[k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
+        }
+      } else {
+        const u32 k1 = (u32)brev(q, lgR);
+        u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
+        const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+        u32* rx = gX + ((long long)q << LGC) + o;
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
+          m = shoup(m, gam, PK<P>::p);
+        }
+      }
+    }
+  }
+}
+
+template <int LGC, bool SMALL>
+__global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
+  switch (blockIdx.y) {
+    case 0: row_body<0, LGC, SMALL>(job, tab, lnr); break;
+    case 1: row_body<1, LGC, SMALL>(job, tab, lnr); break;
+    default: row_body<2, LGC, SMALL>(job, tab, lnr); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column passes.  CTA: CT = 2^lct adjacent columns x R rows, interleaved in
+// smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
+// broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
+// scaled residues.
+template <int P, int LGR>
+__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int CT = 1 << lct;
+  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
+  const int lgC = job.lgC;
+  const long long L = 1ll << job.lg;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
+  const long long kv = op ? job.kX : job.kA;
+  const u32 mask = op ? job.maskX : job.maskA;
+  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
+  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
+
+  if constexpr (PP.n == 1) {
+    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
+      u32 v[1][1 << LGR];
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k)
+        v[0][k] = shoup(fetch_word(src, ((long long)k << lgC) + c0 + t, kv, mask), 1u,
+                        PK<P>::one_sh, PK<P>::p);
+      dif_ct<P, LGR, 1>(v);
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) dst[((long long)k << lgC) + c0 + t] = v[0][k];
+    }
+  } else {
+    // operand rows >= R/2 are all zero when kv <= L/2 (always for the hash):
+    // skip their loads and turn the first DIF stage into one multiply
+    const bool half = kv <= (L >> 1);
+    const int lim = (int)(kv < L ? kv : L);  // words with index < lim are loaded
+    const int ilast = (int)kv - 1;
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      const int col = c0 + t;
+      u32 v[1][1 << RS0];
+      if (half) {
+#pragma unroll
+        for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
+          const int gi = ((o + (k << SLO0)) << lgC) + col;
+          u32 w = gi < lim ? __ldg(src + gi) : 0u;
+          w &= gi == ilast ? mask : 0xFFFFFFFFu;
+          v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+        }
+        dif_rt_half<P, RS0, SLO0>(v, twf + o);
+      } else {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const int gi = ((o + (k << SLO0)) << lgC) + col;
+          u32 w = gi < lim ? __ldg(src + gi) : 0u;
+          w &= gi == ilast ? mask : 0xFFFFFFFFu;
+          v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+        }
+        dif_rt<P, RS0, SLO0, 1>(v, twf + o);
+      }
+      const int base = sm_idx(o) * CT + t;
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) smem[base + k * sm_step(SLO0) * CT] = v[0][k];
+    }
+    __syncthreads();
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
+        const int t = task & (CT - 1), g = task >> lct;
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
+        u32 v[1][1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[0][k] = smem[base + k * sm_step(SLO1) * CT];
+        dif_rt<P, RS1, SLO1, 1>(v, twf + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[0][k];
+      }
+      __syncthreads();
+    }
+    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
+      const int t = task & (CT - 1), g = task >> lct;
+      const int base = (33 * g) * CT + t;
+      u32 v[1][32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[0][k] = smem[base + k * CT];
+      dif_ct<P, 5, 1>(v);
+      u32* d = dst + ((long long)(g << 5) << lgC) + c0 + t;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) d[(long long)k << lgC] = v[0][k];
+    }
+  }
+}
+
+template <int P, int LGR>
+__device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR);
+  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int CT = 1 << lct;
+  const int b = blockIdx.z;
+  const int lgC = job.lgC;
+  const long long L = 1ll << job.lg;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
+  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
+  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
+  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
+
+  if constexpr (PP.n == 1) {
+    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
+      u32 v[1 << LGR];
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) v[k] = src[((long long)k << lgC) + c0 + t];
+      dit_ct<P, LGR>(v);
+#pragma unroll
+      for (int k = 0; k < (1 << LGR); ++k) {
+        const long long gi = ((long long)k << lgC) + c0 + t;
+        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+      }
+    }
+  } else {
+    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
+      const int t = task & (CT - 1), g = task >> lct;
+      const u32* s = src + ((long long)(g << 5) << lgC) + c0 + t;
+      u32 v[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = s[(long long)k << lgC];
+      dit_ct<P, 5>(v);
+      const int base = (33 * g) * CT + t;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) smem[base + k * CT] = v[k];
+    }
+    __syncthreads();
+    if constexpr (PP.n == 3) {
+      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
+      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
+        const int t = task & (CT - 1), g = task >> lct;
+        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
+        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
+        u32 v[1 << RS1];
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) v[k] = smem[base + k * sm_step(SLO1) * CT];
+        dit_rt<P, RS1, SLO1>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[k];
+      }
+      __syncthreads();
+    }
+    // residues are needed only below nRes; when nRes <= L/2 the top DIT stage
+    // produces just its lower half
+    const bool half = job.nRes <= (L >> 1);
+    const int nres = (int)(job.nRes < L ? job.nRes : L);
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      const int base = sm_idx(o) * CT + t;
+      u32 v[1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) v[k] = smem[base + k * sm_step(SLO0) * CT];
+      if (half) {
+        dit_rt_half<P, RS0, SLO0>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
+          const int gi = ((o + (k << SLO0)) << lgC) + c0 + t;
+          if (gi < nres) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+        }
+      } else {
+        dit_rt<P, RS0, SLO0>(v, twi + o);
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const int gi = ((o + (k << SLO0)) << lgC) + c0 + t;
+          if (gi < nres) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+        }
+      }
+    }
+  }
+}
+
+template <int LGR>
+__global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: col_fwd_body<0, LGR>(job, tab, lct); break;
+    case 1: col_fwd_body<1, LGR>(job, tab, lct); break;
+    default: col_fwd_body<2, LGR>(job, tab, lct); break;
+  }
+}
+template <int LGR>
+__global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: col_inv_body<0, LGR>(job, tab, lct); break;
+    case 1: col_inv_body<1, LGR>(job, tab, lct); break;
+    default: col_inv_body<2, LGR>(job, tab, lct); break;
+  }
+}
+
+
+}  // namespace pab
+
+// one translation unit per size: defines conv_kernels_<LG>()
+#define PAB_DEFINE_CONV(LG)                                                          \
+  namespace pab {                                                                    \
+  ConvKernels conv_kernels_##LG() {                                                  \
+    ConvKernels k;                                                                   \
+    k.row = k_row<LG, false>;                                                        \
+    k.row_small = k_row<LG, true>;                                                   \
+    k.col_fwd = (LG >= 6) ? (ConvKernel)k_col_fwd<(LG >= 6 ? LG : 6)> : nullptr;     \
+    k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<(LG >= 6 ? LG : 6)> : nullptr;     \
+    return k;                                                                        \
+  }                                                                                  \
+  }

@@ -1,0 +1,3 @@
+// Instantiates the conv kernels for 2^1-point row/column transforms.
+#include "conv_kernels.cuh"
+PAB_DEFINE_CONV(1)

@@ -200,6 +200,32 @@ __device__ __forceinline__ void dif_rt(u32 (&v)[NV][1 << RS], const uint2* __res
   });
 }
 
+// As dif_rt, but the upper half of the inputs (k >= 2^(RS-1)) is known to be
+// zero (zero-padded operand): the first stage is y = x * w, x unchanged.
+template <int P, int RS, int SLO>
+__device__ __forceinline__ void dif_rt_half(u32 (&v)[1][1 << RS], const uint2* __restrict__ two) {
+  constexpr int H = 1 << (RS - 1);
+  sfor<H>([&](auto k_) {
+    constexpr int k = decltype(k_)::value;
+    constexpr int off = (1 << (RS - 1 + SLO)) + (k << SLO);
+    const uint2 w = __ldg(two + off);
+    v[0][k + H] = v[0][k] * w.x - __umulhi(v[0][k], w.y) * PK<P>::p;
+  });
+  sfor<RS - 1>([&](auto st_) {
+    constexpr int st = decltype(st_)::value + 1;
+    constexpr int sg = RS - 1 - st;
+    constexpr int hr = 1 << sg;
+    sfor<(1 << RS)>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      if constexpr ((k & hr) == 0) {
+        constexpr int off = (1 << (sg + SLO)) + ((k & (hr - 1)) << SLO);
+        const uint2 w = __ldg(two + off);
+        bf_dif<P>(v[0][k], v[0][k + hr], w.x, w.y);
+      }
+    });
+  });
+}
+
 // DIT over stages SLO .. SLO+RS-1 with table (inverse) twiddles; two = tw + o.
 template <int P, int RS, int SLO>
 __device__ __forceinline__ void dit_rt(u32 (&v)[1 << RS], const uint2* __restrict__ two) {
@@ -214,6 +240,32 @@ __device__ __forceinline__ void dit_rt(u32 (&v)[1 << RS], const uint2* __restric
         bf_dit<P>(v[k], v[k + hr], w.x, w.y);
       }
     });
+  });
+}
+
+// As dit_rt, but only the lower half of the outputs (k < 2^(RS-1)) is needed:
+// the last stage computes x + w*y only.
+template <int P, int RS, int SLO>
+__device__ __forceinline__ void dit_rt_half(u32 (&v)[1 << RS], const uint2* __restrict__ two) {
+  sfor<RS - 1>([&](auto st_) {
+    constexpr int st = decltype(st_)::value;
+    constexpr int hr = 1 << st;
+    sfor<(1 << RS)>([&](auto k_) {
+      constexpr int k = decltype(k_)::value;
+      if constexpr ((k & hr) == 0) {
+        constexpr int off = (1 << (st + SLO)) + ((k & (hr - 1)) << SLO);
+        const uint2 w = __ldg(two + off);
+        bf_dit<P>(v[k], v[k + hr], w.x, w.y);
+      }
+    });
+  });
+  constexpr int H = 1 << (RS - 1);
+  sfor<H>([&](auto k_) {
+    constexpr int k = decltype(k_)::value;
+    constexpr int off = (1 << (RS - 1 + SLO)) + (k << SLO);
+    const uint2 w = __ldg(two + off);
+    const u32 a = red(v[k], PK<P>::two_p);
+    v[k] = a + (v[k + H] * w.x - __umulhi(v[k + H], w.y) * PK<P>::p);
   });
 }
 

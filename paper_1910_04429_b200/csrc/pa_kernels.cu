@@ -19,8 +19,7 @@
 #include <string>
 #include <vector>
 
-#include "ntt_core.cuh"
-#include "pa_kernels.cuh"
+#include "conv_kernels.cuh"
 
 namespace pab {
 
@@ -106,10 +105,6 @@ void upload_constants(const PrimeInfo* primes, const CrtConst& crt) {
   cudaMemcpyToSymbol(c_crt, &crt, sizeof(CrtConst));
 }
 
-__device__ __forceinline__ int brev(int x, int bits) {
-  return bits == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - bits));
-}
-
 // ---------------------------------------------------------------------------
 // pack / unpack (MSF byte order or unaligned blocks only)
 
@@ -176,398 +171,6 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
 }
 
 // ---------------------------------------------------------------------------
-// operand word fetch: zero beyond the valid words, mask the last one
-__device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long gi, long long kv,
-                                          u32 mask) {
-  if (gi >= kv) return 0u;
-  const u32 w = __ldg(src + gi);
-  return gi == kv - 1 ? (w & mask) : w;
-}
-
-// four-step twiddle seed w_L^e * 2^32 (Montgomery form, lazy [0, 2p)), e < L
-template <int P>
-__device__ __forceinline__ u32 tw_seed(const PlanTables& tab, int dir, u32 e) {
-  const int off = (P * 2 + dir) * kTwN;
-  const u32 lo = __ldg(&tab.tlo_m[off + (e & (kTwN - 1))]);
-  const uint2 hi = __ldg(&tab.thi[off + (e >> kTwLg)]);
-  return shoup(lo, hi, PK<P>::p);
-}
-
-// ---------------------------------------------------------------------------
-// Row pass.  CTA: NR = 2^lnr rows of one (block, prime); smem holds the NR
-// c-rows (A) then the NR x-rows (X), each sm_len(LGC) words.
-// SMALL (lgR == 0): the row is the whole transform; read the operand words,
-// write scaled residues.
-template <int P, int LGC, bool SMALL>
-__device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& tab, int lnr) {
-  extern __shared__ u32 smem[];
-  constexpr PassPlan PP = pass_plan(LGC);
-  constexpr int T = sm_len(LGC);
-  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
-  const int NR = 1 << lnr;
-  const int b = blockIdx.z;
-  const int q0 = blockIdx.x << lnr;
-  const int lgR = job.lgR;
-  const long long L = 1ll << job.lg;
-  u32* sA = smem;
-  u32* sX = smem + NR * T;
-  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
-  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
-  u32* gA = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;  // also the residue slot
-  u32* gX = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
-  const u32* wA = job.srcA + (long long)b * job.src_stride;
-  const u32* wX = job.srcX + (long long)b * job.src_stride;
-
-  // ---- pass 0: global -> (twiddle) -> DIF top stages -> smem (A and X share twiddles)
-  if constexpr (PP.n > 1) {
-    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
-      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
-      const int q = q0 + row;
-      u32 v[2][1 << RS0];
-      if constexpr (SMALL) {
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          const long long gi = o + (k << SLO0);
-          v[0][k] = shoup(fetch_word(wA, gi, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
-          v[1][k] = shoup(fetch_word(wX, gi, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
-        }
-      } else {
-        const u32* ra = gA + ((long long)q << LGC) + o;
-        const u32* rx = gX + ((long long)q << LGC) + o;
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          v[0][k] = ra[k << SLO0];
-          v[1][k] = rx[k << SLO0];
-        }
-        const u32 k1 = (u32)brev(q, lgR);
-        u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
-        const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          v[0][k] = mont<P>(v[0][k], m);
-          v[1][k] = mont<P>(v[1][k], m);
-          m = shoup(m, gam, PK<P>::p);
-        }
-      }
-      dif_rt<P, RS0, SLO0, 2>(v, twf + o);
-      const int base = row * T + sm_idx(o);
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) {
-        sA[base + k * sm_step(SLO0)] = v[0][k];
-        sX[base + k * sm_step(SLO0)] = v[1][k];
-      }
-    }
-    __syncthreads();
-  }
-  // ---- pass 1 (middle), forward, A and X
-  if constexpr (PP.n == 3) {
-    constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
-    constexpr int LGG = LGC - RS1;  // groups per row (log2)
-    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
-      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
-      const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
-      const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
-      u32 v[2][1 << RS1];
-#pragma unroll
-      for (int k = 0; k < (1 << RS1); ++k) {
-        v[0][k] = sA[base + k * sm_step(SLO1)];
-        v[1][k] = sX[base + k * sm_step(SLO1)];
-      }
-      dif_rt<P, RS1, SLO1, 2>(v, twf + o);
-#pragma unroll
-      for (int k = 0; k < (1 << RS1); ++k) {
-        sA[base + k * sm_step(SLO1)] = v[0][k];
-        sX[base + k * sm_step(SLO1)] = v[1][k];
-      }
-    }
-    __syncthreads();
-  }
-  // ---- last DIF pass (lowest stages) + pointwise + first DIT pass
-  constexpr int RSL = PP.rs[PP.n - 1];
-  {
-    constexpr int LGG = LGC - RSL;
-    for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
-      const int row = task >> LGG, g = task & ((1 << LGG) - 1);
-      u32 a[1][1 << RSL], x[1][1 << RSL];
-      int base = 0;
-      if constexpr (PP.n == 1) {  // whole transform in registers, straight from global
-        const int q = q0 + row;
-        if constexpr (SMALL) {
-#pragma unroll
-          for (int k = 0; k < (1 << RSL); ++k) {
-            a[0][k] = shoup(fetch_word(wA, k, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
-            x[0][k] = shoup(fetch_word(wX, k, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
-          }
-        } else {
-          const u32 k1 = (u32)brev(q, lgR);
-          u32 m = tw_seed<P>(tab, 0, 0u);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
-#pragma unroll
-          for (int k = 0; k < (1 << RSL); ++k) {
-            a[0][k] = mont<P>(gA[((long long)q << LGC) + k], m);
-            x[0][k] = mont<P>(gX[((long long)q << LGC) + k], m);
-            m = shoup(m, gam, PK<P>::p);
-          }
-        }
-      } else {
-        base = row * T + sm_idx(g << RSL);
-#pragma unroll
-        for (int k = 0; k < (1 << RSL); ++k) a[0][k] = sA[base + k];
-#pragma unroll
-        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = sX[base + k];
-      }
-      dif_ct<P, RSL, 1>(a);
-      dif_ct<P, RSL, 1>(x);
-#pragma unroll
-      for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
-      dit_ct<P, RSL>(x[0]);
-      if constexpr (PP.n == 1) {
-        const int q = q0 + row;
-        if constexpr (SMALL) {
-#pragma unroll
-          for (int k = 0; k < (1 << RSL); ++k)
-            if (k < job.nRes)
-              gA[k] = red(shoup(x[0][k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
-        } else {
-          const u32 k1 = (u32)brev(q, lgR);
-          u32 m = tw_seed<P>(tab, 1, 0u);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
-#pragma unroll
-          for (int k = 0; k < (1 << RSL); ++k) {
-            gX[((long long)q << LGC) + k] = mont<P>(red(x[0][k], PK<P>::two_p), m);
-            m = shoup(m, gam, PK<P>::p);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < (1 << RSL); ++k) sX[base + k] = x[0][k];
-      }
-    }
-  }
-  if constexpr (PP.n > 1) {
-    __syncthreads();
-    // ---- pass 1 inverse (X)
-    if constexpr (PP.n == 3) {
-      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
-      constexpr int LGG = LGC - RS1;
-      for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
-        const int row = task >> LGG, g = task & ((1 << LGG) - 1);
-        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
-        const int base = row * T + sm_idx((blk << (SLO1 + RS1)) + o);
-        u32 v[1 << RS1];
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) v[k] = sX[base + k * sm_step(SLO1)];
-        dit_rt<P, RS1, SLO1>(v, twi + o);
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) sX[base + k * sm_step(SLO1)] = v[k];
-      }
-      __syncthreads();
-    }
-    // ---- pass 0 inverse (X) -> inverse twiddle -> global (or scaled residues)
-    for (int task = threadIdx.x; task < (NR << SLO0); task += blockDim.x) {
-      const int row = task >> SLO0, o = task & ((1 << SLO0) - 1);
-      const int q = q0 + row;
-      const int base = row * T + sm_idx(o);
-      u32 v[1 << RS0];
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) v[k] = sX[base + k * sm_step(SLO0)];
-      dit_rt<P, RS0, SLO0>(v, twi + o);
-      if constexpr (SMALL) {
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          const long long gi = o + (k << SLO0);
-          if (gi < job.nRes)
-            gA[gi] = red(shoup(v[k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
-        }
-      } else {
-        const u32 k1 = (u32)brev(q, lgR);
-        u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
-        const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
-        u32* rx = gX + ((long long)q << LGC) + o;
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
-          m = shoup(m, gam, PK<P>::p);
-        }
-      }
-    }
-  }
-}
-
-template <int LGC, bool SMALL>
-__global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
-  switch (blockIdx.y) {
-    case 0: row_body<0, LGC, SMALL>(job, tab, lnr); break;
-    case 1: row_body<1, LGC, SMALL>(job, tab, lnr); break;
-    default: row_body<2, LGC, SMALL>(job, tab, lnr); break;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Column passes.  CTA: CT = 2^lct adjacent columns x R rows, interleaved in
-// smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
-// broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
-// scaled residues.
-template <int P, int LGR>
-__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
-  extern __shared__ u32 smem[];
-  constexpr PassPlan PP = pass_plan(LGR);
-  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
-  const int CT = 1 << lct;
-  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
-  const int lgC = job.lgC;
-  const long long L = 1ll << job.lg;
-  const int c0 = blockIdx.x << lct;
-  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
-  const long long kv = op ? job.kX : job.kA;
-  const u32 mask = op ? job.maskX : job.maskA;
-  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
-  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
-
-  if constexpr (PP.n == 1) {
-    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
-      u32 v[1][1 << LGR];
-#pragma unroll
-      for (int k = 0; k < (1 << LGR); ++k)
-        v[0][k] = shoup(fetch_word(src, ((long long)k << lgC) + c0 + t, kv, mask), 1u,
-                        PK<P>::one_sh, PK<P>::p);
-      dif_ct<P, LGR, 1>(v);
-#pragma unroll
-      for (int k = 0; k < (1 << LGR); ++k) dst[((long long)k << lgC) + c0 + t] = v[0][k];
-    }
-  } else {
-    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
-      const int t = task & (CT - 1), o = task >> lct;
-      u32 v[1][1 << RS0];
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) {
-        const long long gi = ((long long)(o + (k << SLO0)) << lgC) + c0 + t;
-        v[0][k] = shoup(fetch_word(src, gi, kv, mask), 1u, PK<P>::one_sh, PK<P>::p);
-      }
-      dif_rt<P, RS0, SLO0, 1>(v, twf + o);
-      const int base = sm_idx(o) * CT + t;
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) smem[base + k * sm_step(SLO0) * CT] = v[0][k];
-    }
-    __syncthreads();
-    if constexpr (PP.n == 3) {
-      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
-      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
-        const int t = task & (CT - 1), g = task >> lct;
-        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
-        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
-        u32 v[1][1 << RS1];
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) v[0][k] = smem[base + k * sm_step(SLO1) * CT];
-        dif_rt<P, RS1, SLO1, 1>(v, twf + o);
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[0][k];
-      }
-      __syncthreads();
-    }
-    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
-      const int t = task & (CT - 1), g = task >> lct;
-      const int base = (33 * g) * CT + t;
-      u32 v[1][32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[0][k] = smem[base + k * CT];
-      dif_ct<P, 5, 1>(v);
-      u32* d = dst + ((long long)(g << 5) << lgC) + c0 + t;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) d[(long long)k << lgC] = v[0][k];
-    }
-  }
-}
-
-template <int P, int LGR>
-__device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
-  extern __shared__ u32 smem[];
-  constexpr PassPlan PP = pass_plan(LGR);
-  constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
-  const int CT = 1 << lct;
-  const int b = blockIdx.z;
-  const int lgC = job.lgC;
-  const long long L = 1ll << job.lg;
-  const int c0 = blockIdx.x << lct;
-  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
-  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
-  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
-  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
-
-  if constexpr (PP.n == 1) {
-    for (int t = threadIdx.x; t < CT; t += blockDim.x) {
-      u32 v[1 << LGR];
-#pragma unroll
-      for (int k = 0; k < (1 << LGR); ++k) v[k] = src[((long long)k << lgC) + c0 + t];
-      dit_ct<P, LGR>(v);
-#pragma unroll
-      for (int k = 0; k < (1 << LGR); ++k) {
-        const long long gi = ((long long)k << lgC) + c0 + t;
-        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
-      }
-    }
-  } else {
-    for (int task = threadIdx.x; task < (CT << (LGR - 5)); task += blockDim.x) {
-      const int t = task & (CT - 1), g = task >> lct;
-      const u32* s = src + ((long long)(g << 5) << lgC) + c0 + t;
-      u32 v[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = s[(long long)k << lgC];
-      dit_ct<P, 5>(v);
-      const int base = (33 * g) * CT + t;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) smem[base + k * CT] = v[k];
-    }
-    __syncthreads();
-    if constexpr (PP.n == 3) {
-      constexpr int RS1 = PP.rs[1], SLO1 = PP.slo[1];
-      for (int task = threadIdx.x; task < (CT << (LGR - RS1)); task += blockDim.x) {
-        const int t = task & (CT - 1), g = task >> lct;
-        const int o = g & ((1 << SLO1) - 1), blk = g >> SLO1;
-        const int base = sm_idx((blk << (SLO1 + RS1)) + o) * CT + t;
-        u32 v[1 << RS1];
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) v[k] = smem[base + k * sm_step(SLO1) * CT];
-        dit_rt<P, RS1, SLO1>(v, twi + o);
-#pragma unroll
-        for (int k = 0; k < (1 << RS1); ++k) smem[base + k * sm_step(SLO1) * CT] = v[k];
-      }
-      __syncthreads();
-    }
-    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
-      const int t = task & (CT - 1), o = task >> lct;
-      const int base = sm_idx(o) * CT + t;
-      u32 v[1 << RS0];
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) v[k] = smem[base + k * sm_step(SLO0) * CT];
-      dit_rt<P, RS0, SLO0>(v, twi + o);
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) {
-        const long long gi = ((long long)(o + (k << SLO0)) << lgC) + c0 + t;
-        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
-      }
-    }
-  }
-}
-
-template <int LGR>
-__global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: col_fwd_body<0, LGR>(job, tab, lct); break;
-    case 1: col_fwd_body<1, LGR>(job, tab, lct); break;
-    default: col_fwd_body<2, LGR>(job, tab, lct); break;
-  }
-}
-template <int LGR>
-__global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: col_inv_body<0, LGR>(job, tab, lct); break;
-    case 1: col_inv_body<1, LGR>(job, tab, lct); break;
-    default: col_inv_body<2, LGR>(job, tab, lct); break;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Carry: CRT of the three residues, overlap-add of the 96-bit coefficients at
 // 32-bit stride, + D, carry-lookahead scan (decoupled look-back across tiles),
 // mask to n_mod_bits, shift right, write the key.
@@ -610,186 +213,292 @@ __device__ __forceinline__ void crt3(u32 r0, u32 r1, u32 r2, u32& w0, u32& w1, u
   w2 = (u32)prod_hi;
 }
 
-__global__ void __launch_bounds__(kCarryThreads) k_carry(ConvJob job) {
-  __shared__ u32 s_tile;
-  __shared__ u32 s_wq[kCarryThreads / 32], s_wt[kCarryThreads / 32];
-  __shared__ u32 s_cin;
-  const int b = blockIdx.y;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&job.tile_ctr[b], 1u);
-  __syncthreads();
-  const int tile = (int)s_tile;
+__device__ __forceinline__ void crt_at(const u32* r0, const u32* r1, const u32* r2, long long k,
+                                       long long nres, u32& w0, u32& w1, u32& w2) {
+  if (k >= 0 && k < nres) {
+    crt3(__ldg(r0 + k), __ldg(r1 + k), __ldg(r2 + k), w0, w1, w2);
+  } else {
+    w0 = w1 = w2 = 0u;
+  }
+}
+
+// Warp-striped carry: a CTA tile is kCarryWarps * kCarryRows rows of 32 words;
+// lane j of warp w holds words tile_base + (w*kCarryRows + i)*32 + j, so every
+// load/store of a row is one coalesced 128-byte access.  Within a row, the
+// multi-bit carries (< 8) are folded one word up and the remaining 1-bit
+// carries resolved with a ballot carry-lookahead: with G = ballot(overflow),
+// P = ballot(word == ~0), the carries into all lanes are (A+B)^A^B for
+// A = G|P, B = G.  Rows chain sequentially inside the warp; warps and tiles
+// compose carry functions c -> q + (c >= t).
+struct CarrySmem {
+  u32 tile, cin;
+  u32 wq[kCarryWarps], wt[kCarryWarps];
+  u32 first[kCarryWarps];
+};
+
+// Resolve one row: s = column sums (u64) of this lane's word, cin_row = carry
+// into lane 0 (< 2^32).  Returns final word; updates cin_row to the row's
+// carry-out (into the next row), computes all-ones ballot.
+__device__ __forceinline__ u32 carry_row(u64 s, u32& cin_row, unsigned& ones_mask) {
+  const int lane = threadIdx.x & 31;
+  const u32 lo = (u32)s, hi = (u32)(s >> 32);
+  const u32 hprev = __shfl_up_sync(0xFFFFFFFFu, hi, 1);
+  const u32 hlast = __shfl_sync(0xFFFFFFFFu, hi, 31);
+  const u32 add = lane ? hprev : cin_row;
+  const u32 u = lo + add;
+  const bool g = u < lo;
+  const unsigned G = __ballot_sync(0xFFFFFFFFu, g);
+  const unsigned Pm = __ballot_sync(0xFFFFFFFFu, u == 0xFFFFFFFFu);
+  const unsigned A = G | Pm, B = G;
+  const u64 sum = (u64)A + B;
+  const unsigned carries = ((unsigned)sum ^ A ^ B);
+  const u32 kout = (u32)(sum >> 32);
+  const u32 t = u + ((carries >> lane) & 1u);
+  ones_mask = __ballot_sync(0xFFFFFFFFu, t == 0xFFFFFFFFu);
+  cin_row = hlast + kout;
+  return t;
+}
+
+// One tile of block b; LOOKBACK: carry-in via decoupled look-back, else cin_seq.
+// Returns the carry out of the tile.
+template <bool LOOKBACK>
+__device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int b, int tile,
+                                          u32 cin_seq) {
+  constexpr int NR = kCarryRows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long L = 1ll << job.lg;
   const u32* res0 = job.buf + (((long long)b * 2 + 0) * 3 + 0) * L;
   const u32* res1 = res0 + L;
   const u32* res2 = res1 + L;
   const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
-  const long long w0 = (long long)tile * kCarryTile + (long long)threadIdx.x * kCarryItems;
+  const long long tbase = (long long)tile * kCarryTile;
+  const long long wb = tbase + (long long)warp * NR * 32;  // first word of this warp
+  const long long nres = job.nRes;
 
-  // column sums S[j] for words w0 .. w0+8
-  u64 S[kCarryItems + 1];
-  {
-    u32 A0[kCarryItems + 3], A1[kCarryItems + 3], A2[kCarryItems + 3];
+  // issue every load of the tile first (memory-level parallelism), then CRT
+  u32 V0[NR], V1[NR], V2[NR], DV[NR];
+  const long long kd = dw ? job.kD : 0;
 #pragma unroll
-    for (int j = 0; j < kCarryItems + 3; ++j) {
-      const long long k = w0 - 2 + j;
-      if (k >= 0 && k < job.nRes) {
-        crt3(__ldg(&res0[k]), __ldg(&res1[k]), __ldg(&res2[k]), A0[j], A1[j], A2[j]);
-      } else {
-        A0[j] = A1[j] = A2[j] = 0u;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j <= kCarryItems; ++j) {
-      const long long w = w0 + j;
-      const u32 d = dw ? fetch_word(dw, w, job.kD, job.maskD) : 0u;
-      S[j] = (u64)A0[j + 2] + A1[j + 1] + A2[j] + d;
-    }
+  for (int i = 0; i < NR; ++i) {
+    const long long k = wb + i * 32 + lane;
+    const bool ok = k < nres;
+    V0[i] = ok ? __ldg(res0 + k) : 0u;
+    V1[i] = ok ? __ldg(res1 + k) : 0u;
+    V2[i] = ok ? __ldg(res2 + k) : 0u;
+    DV[i] = k < kd ? __ldg(dw + k) : 0u;
   }
-  // local carry function
+  // virtual row -1 (lanes 30, 31 hold coefficients wb-2, wb-1)
+  u32 P1 = 0, P2 = 0;
+  {
+    const long long k = wb - 32 + lane;
+    const bool ok = lane >= 30 && k >= 0 && k < nres;
+    const u32 q0 = ok ? __ldg(res0 + k) : 0u, q1 = ok ? __ldg(res1 + k) : 0u,
+              q2 = ok ? __ldg(res2 + k) : 0u;
+    u32 x0;
+    crt3(q0, q1, q2, x0, P1, P2);
+    if (!ok) P1 = P2 = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const long long k = wb + i * 32 + lane;
+    const bool ok = k < nres;
+    crt3(V0[i], V1[i], V2[i], V0[i], V1[i], V2[i]);
+    if (!ok) V0[i] = V1[i] = V2[i] = 0u;
+    if (k == kd - 1) DV[i] &= job.maskD;
+  }
+  // column sums S_k = V0[k] + V1[k-1] + V2[k-2] + d[k]
+  u64 S[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const u32 p1row = i ? V1[i - 1] : P1, p2row = i ? V2[i - 1] : P2;
+    const u32 a1 = __shfl_up_sync(0xFFFFFFFFu, V1[i], 1);
+    const u32 b1 = __shfl_sync(0xFFFFFFFFu, p1row, 31);
+    const u32 a2 = __shfl_up_sync(0xFFFFFFFFu, V2[i], 2);
+    const u32 b2 = __shfl_sync(0xFFFFFFFFu, p2row, 30 + (lane & 1));
+    S[i] = (u64)V0[i] + (lane ? a1 : b1) + (lane >= 2 ? a2 : b2) + DV[i];
+  }
+  // warp carry function (carry-in 0)
   CarryFn f;
   {
     u32 c = 0;
-    u32 first = 0;
     bool allones = true;
+    u32 first = 0;
 #pragma unroll
-    for (int j = 0; j < kCarryItems; ++j) {
-      const u64 s = S[j] + c;
-      const u32 t = (u32)s;
-      c = (u32)(s >> 32);
-      if (j == 0) first = t;
-      else allones &= (t == 0xFFFFFFFFu);
+    for (int i = 0; i < NR; ++i) {
+      unsigned ones;
+      const u32 t = carry_row(S[i], c, ones);
+      if (i == 0) {
+        first = __shfl_sync(0xFFFFFFFFu, t, 0);
+        ones |= 1u;
+      }
+      allones &= (ones == 0xFFFFFFFFu);
     }
     f.id = false;
     f.q = c;
     f.t = (allones && first != 0u) ? (0u - first) : kInf;
   }
-  // warp inclusive scan
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  CarryFn inc = f;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    CarryFn o;
-    o.q = __shfl_up_sync(0xFFFFFFFFu, inc.q, d);
-    o.t = __shfl_up_sync(0xFFFFFFFFu, inc.t, d);
-    o.id = false;
-    if (lane >= d) inc = cf_compose(inc, o);
-  }
-  CarryFn excl;
-  excl.q = __shfl_up_sync(0xFFFFFFFFu, inc.q, 1);
-  excl.t = __shfl_up_sync(0xFFFFFFFFu, inc.t, 1);
-  excl.id = (lane == 0);
-  if (lane == 31) {
-    s_wq[warp] = inc.q;
-    s_wt[warp] = inc.t;
+  if (lane == 0) {
+    sm.wq[warp] = f.q;
+    sm.wt[warp] = f.t;
   }
   __syncthreads();
-  // prefix of earlier warps, and the tile aggregate
-  CarryFn wpre{0, 0, true};
-  CarryFn agg{0, 0, true};
+  CarryFn wpre{0, 0, true}, agg{0, 0, true};
 #pragma unroll
-  for (int w = 0; w < kCarryThreads / 32; ++w) {
-    CarryFn fw{s_wq[w], s_wt[w], false};
+  for (int w = 0; w < kCarryWarps; ++w) {
+    const CarryFn fw{sm.wq[w], sm.wt[w], false};
     if (w < warp) wpre = cf_compose(fw, wpre);
     agg = cf_compose(fw, agg);
   }
-  excl = cf_compose(excl, wpre);
-
-  // decoupled look-back over the tiles of this block
-  if (threadIdx.x == 0) {
-    volatile unsigned long long* st = job.tile_state + (long long)b * job.tiles;
-    u32 cin;
-    if (tile == 0) {
-      cin = 0;
-    } else {
-      st[tile] = (1ull << 62) | ((unsigned long long)agg.q << 32) | agg.t;
-      CarryFn F{0, 0, true};
-      int j = tile - 1;
-      while (true) {
-        const unsigned long long v = st[j];
-        const u32 flag = (u32)(v >> 62);
-        if (flag == 0) continue;
-        if (flag == 2) {
-          cin = cf_apply(F, (u32)((v >> 32) & 0xFFu));
-          break;
+  // carry into the tile
+  if (LOOKBACK) {
+    if (warp == 0) {  // decoupled look-back: 32 predecessor tiles per probe
+      volatile unsigned long long* st = job.tile_state + (long long)b * job.tiles;
+      u32 cin = 0;
+      if (tile > 0) {
+        if (lane == 0) st[tile] = (1ull << 62) | ((unsigned long long)agg.q << 32) | agg.t;
+        CarryFn F{0, 0, true};
+        int base = tile - 1;
+        while (true) {
+          const int j = base - lane;
+          const unsigned long long v = j >= 0 ? st[j] : (2ull << 62);
+          const u32 flag = (u32)(v >> 62);
+          const unsigned zero = __ballot_sync(0xFFFFFFFFu, flag == 0);
+          const unsigned pre = __ballot_sync(0xFFFFFFFFu, flag == 2);
+          const int first = pre ? __ffs(pre) - 1 : 32;
+          const unsigned need = first == 32 ? 0xFFFFFFFFu : ((2u << first) - 1u);
+          if (zero & need) continue;
+          const u32 q = (u32)((v >> 32) & 0xFFu), t = (u32)v;
+          for (int i = 0; i < first; ++i) {
+            const CarryFn g{__shfl_sync(0xFFFFFFFFu, q, i), __shfl_sync(0xFFFFFFFFu, t, i), false};
+            F = cf_compose(F, g);
+          }
+          if (first < 32) {
+            cin = cf_apply(F, __shfl_sync(0xFFFFFFFFu, q, first));
+            break;
+          }
+          base -= 32;
         }
-        CarryFn g{(u32)((v >> 32) & 0xFFu), (u32)v, false};
-        F = cf_compose(F, g);
-        --j;
+      }
+      if (lane == 0) {
+        st[tile] = (2ull << 62) | ((unsigned long long)cf_apply(agg, cin) << 32);
+        sm.cin = cin;
       }
     }
-    const u32 cout = cf_apply(agg, cin);
-    st[tile] = (2ull << 62) | ((unsigned long long)cout << 32);
-    s_cin = cin;
+  } else if (threadIdx.x == 0) {
+    sm.cin = cin_seq;
   }
   __syncthreads();
-  u32 c = cf_apply(excl, s_cin);
+  const u32 tile_cin = sm.cin;
 
-  // final words, masked
-  u32 T[kCarryItems + 1];
+  // final words with the real carry-in
+  u32 c = cf_apply(wpre, tile_cin);
+  u32 T[NR];
+  const long long nT = job.nT;
+  const long long rbits = job.n_mod_bits - 32ll * (nT - 1);
+  const u32 tmask = rbits >= 32 ? 0xFFFFFFFFu : ((1u << rbits) - 1u);
 #pragma unroll
-  for (int j = 0; j <= kCarryItems; ++j) {
-    const u64 s = S[j] + c;
-    T[j] = (u32)s;
-    c = (u32)(s >> 32);
-    const long long w = w0 + j;
-    if (w >= job.nT) {
-      T[j] = 0u;
-    } else if (w == job.nT - 1) {
-      const long long rb = job.n_mod_bits - 32ll * (job.nT - 1);
-      if (rb < 32) T[j] &= (1u << rb) - 1u;
-    }
+  for (int i = 0; i < NR; ++i) {
+    unsigned ones;
+    T[i] = carry_row(S[i], c, ones);
+    const long long w = wb + i * 32 + lane;
+    T[i] = w >= nT ? 0u : (w == nT - 1 ? (T[i] & tmask) : T[i]);
   }
-  // output words y_j = T >> shift
+  // word after this warp's last word: next warp's first word, or (last warp)
+  // the next tile's first word = S_next + carry
+  if (lane == 0) sm.first[warp] = T[0];
+  u32 nextw = 0;
+  if (warp == kCarryWarps - 1) {
+    const long long k = wb + NR * 32;  // first word of the next tile
+    u32 n0 = 0, n1, n2;
+    if (lane == 0) crt_at(res0, res1, res2, k, nres, n0, n1, n2);
+    n0 = __shfl_sync(0xFFFFFFFFu, n0, 0);
+    const u32 v1 = __shfl_sync(0xFFFFFFFFu, V1[NR - 1], 31);
+    const u32 v2 = __shfl_sync(0xFFFFFFFFu, V2[NR - 1], 30);
+    const u32 dv = dw ? fetch_word(dw, k, job.kD, job.maskD) : 0u;
+    const u64 sn = (u64)n0 + v1 + v2 + dv + c;
+    nextw = (u32)sn;
+    nextw = k >= nT ? 0u : (k == nT - 1 ? (nextw & tmask) : nextw);
+  }
+  __syncthreads();
+  if (warp < kCarryWarps - 1) nextw = sm.first[warp + 1];
+  // output words y_o = (T >> shift), o = w - shift/32
   const long long ws = job.shift >> 5;
   const int sh = (int)(job.shift & 31);
-  if (job.out_words) {
-    u32* out = job.out_words + (long long)b * job.mw;
+  uint8_t* outb = job.out_words ? nullptr : job.out_bytes + (long long)b * job.out_stride;
+  u32* outw = job.out_words ? job.out_words + (long long)b * job.mw : nullptr;
 #pragma unroll
-    for (int j = 0; j < kCarryItems; ++j) {
-      const long long oj = w0 + j - ws;
-      if (oj >= 0 && oj < job.mw) out[oj] = sh ? ((T[j] >> sh) | (T[j + 1] << (32 - sh))) : T[j];
-    }
-  } else {  // LSF bytes, word-aligned block starts
-    uint8_t* out = job.out_bytes + (long long)b * job.out_stride;
-#pragma unroll
-    for (int j = 0; j < kCarryItems; ++j) {
-      const long long oj = w0 + j - ws;
-      if (oj >= 0 && oj < job.mw) {
-        const u32 y = sh ? ((T[j] >> sh) | (T[j + 1] << (32 - sh))) : T[j];
-        if (4 * oj + 4 <= job.rbytes) {
-          reinterpret_cast<u32*>(out)[oj] = y;
-        } else {
-          for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q)
-            out[4 * oj + q] = (uint8_t)(y >> (8 * q));
-        }
+  for (int i = 0; i < NR; ++i) {
+    const u32 up = __shfl_down_sync(0xFFFFFFFFu, T[i], 1);
+    const u32 nx = i + 1 < NR ? T[i + 1] : nextw;
+    const u32 wrap = __shfl_sync(0xFFFFFFFFu, nx, 0);
+    const u32 hiw = lane < 31 ? up : (i + 1 < NR ? wrap : nextw);
+    const long long oj = wb + i * 32 + lane - ws;
+    if (oj >= 0 && oj < job.mw) {
+      const u32 y = sh ? ((T[i] >> sh) | (hiw << (32 - sh))) : T[i];
+      if (outw) {
+        outw[oj] = y;
+      } else if (4 * oj + 4 <= job.rbytes) {
+        reinterpret_cast<u32*>(outb)[oj] = y;
+      } else {
+        for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q) outb[4 * oj + q] = (uint8_t)(y >> (8 * q));
       }
     }
   }
+  const u32 cout = cf_apply(agg, tile_cin);
+  __syncthreads();  // smem reuse by the next tile
+  return cout;
+}
+
+// Decoupled look-back across tiles: one CTA per tile (few, huge blocks).
+__global__ void __launch_bounds__(kCarryThreads) k_carry_lb(ConvJob job) {
+  __shared__ CarrySmem sm;
+  const int b = blockIdx.y;
+  if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
+  __syncthreads();
+  carry_tile<true>(job, sm, b, (int)sm.tile, 0u);
+}
+
+// One CTA per block walking its tiles in order (many blocks): no inter-CTA waits.
+__global__ void __launch_bounds__(kCarryThreads) k_carry_seq(ConvJob job) {
+  __shared__ CarrySmem sm;
+  const int b = blockIdx.y;
+  u32 c = 0;
+  for (int tile = 0; tile < job.tiles; ++tile) c = carry_tile<false>(job, sm, b, tile, c);
 }
 
 // ---------------------------------------------------------------------------
 // dispatch over compile-time transform sizes
 
-typedef void (*ConvKernel)(ConvJob, PlanTables, int);
+#define PAB_DECL(L) ConvKernels conv_kernels_##L();
+PAB_DECL(1) PAB_DECL(2) PAB_DECL(3) PAB_DECL(4) PAB_DECL(5) PAB_DECL(6)
+PAB_DECL(7) PAB_DECL(8) PAB_DECL(9) PAB_DECL(10) PAB_DECL(11) PAB_DECL(12)
+#undef PAB_DECL
 
-static ConvKernel row_kernel(int lg, bool small) {
+static ConvKernels conv_for(int lg) {
   switch (lg) {
-#define PAB_ROW(L) \
-  case L: return small ? k_row<L, true> : k_row<L, false>;
-    PAB_ROW(1) PAB_ROW(2) PAB_ROW(3) PAB_ROW(4) PAB_ROW(5) PAB_ROW(6) PAB_ROW(7) PAB_ROW(8)
-    PAB_ROW(9) PAB_ROW(10) PAB_ROW(11) PAB_ROW(12)
-#undef PAB_ROW
-    default: return nullptr;
+    case 1: return conv_kernels_1();
+    case 2: return conv_kernels_2();
+    case 3: return conv_kernels_3();
+    case 4: return conv_kernels_4();
+    case 5: return conv_kernels_5();
+    case 6: return conv_kernels_6();
+    case 7: return conv_kernels_7();
+    case 8: return conv_kernels_8();
+    case 9: return conv_kernels_9();
+    case 10: return conv_kernels_10();
+    case 11: return conv_kernels_11();
+    case 12: return conv_kernels_12();
+    default: return ConvKernels{nullptr, nullptr, nullptr, nullptr};
   }
 }
+static ConvKernel row_kernel(int lg, bool small) {
+  const ConvKernels k = conv_for(lg);
+  return small ? k.row_small : k.row;
+}
 static ConvKernel col_kernel(int lg, bool inv) {
-  switch (lg) {
-#define PAB_COL(L) \
-  case L: return inv ? k_col_inv<L> : k_col_fwd<L>;
-    PAB_COL(6) PAB_COL(7) PAB_COL(8) PAB_COL(9) PAB_COL(10) PAB_COL(11) PAB_COL(12)
-#undef PAB_COL
-    default: return nullptr;
-  }
+  if (lg < 6) return nullptr;
+  const ConvKernels k = conv_for(lg);
+  return inv ? k.col_inv : k.col_fwd;
 }
 
 static int col_lct(int lgR, int lgC) {
@@ -833,7 +542,11 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
   prof::Scope ps_("k_carry", st);
-  k_carry<<<dim3(job.tiles, job.batch), kCarryThreads, 0, st>>>(job);
+  if (job.batch >= 2 * 148 || job.tiles == 1) {
+    k_carry_seq<<<dim3(1, job.batch), kCarryThreads, 0, st>>>(job);
+  } else {
+    k_carry_lb<<<dim3(job.tiles, job.batch), kCarryThreads, 0, st>>>(job);
+  }
 }
 
 // Opt every dynamic-smem kernel into > 48 KB once per device.

@@ -52,9 +52,10 @@ struct ConvJob {
   int tiles;                   // carry tiles per block
 };
 
-constexpr int kCarryThreads = 256;
-constexpr int kCarryItems = 8;
-constexpr int kCarryTile = kCarryThreads * kCarryItems;
+constexpr int kCarryWarps = 8;                           // warps per carry CTA
+constexpr int kCarryRows = 8;                            // 32-word rows per warp
+constexpr int kCarryThreads = 32 * kCarryWarps;
+constexpr int kCarryTile = 32 * kCarryWarps * kCarryRows;  // words per tile
 
 void upload_constants(const PrimeInfo* primes, const CrtConst& crt);
 void set_kernel_attrs();

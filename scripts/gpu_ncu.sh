@@ -2,7 +2,7 @@ set -e
 cd paper_1910_04429_b200/csrc && make -s 2>&1 | grep -i error || true; cd ../..
 make -s -C oracle
 mkdir -p gpurun_out
-TAG=${TAG:-r1}
+TAG=${1:-r1}
 CMD="python bench.py --steps 3 --warmup 3 --no-extra --no-cpu"
 $CMD > gpurun_out/plain_bench.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch.log 2>&1

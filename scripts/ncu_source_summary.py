@@ -8,9 +8,10 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
                       f"regex:{kern}"], capture_output=True, text=True).stdout
-lines = txt.splitlines()
-rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
-hdr, body = rows[0], rows[1:]
+rows = [r for r in csv.reader(io.StringIO(txt)) if r]
+hdr = next(r for r in rows if r[0] == "Address")
+body = [r for r in rows if r[0] not in ("Address", "Kernel Name") and len(r) >= len(hdr) - 1]
+body = [r + [""] * (len(hdr) - len(r)) for r in body]
 H = {h: i for i, h in enumerate(hdr)}
 num = lambda r, k: float(r[H[k]] or 0) if r[H[k]] not in ("-", "") else 0.0
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]

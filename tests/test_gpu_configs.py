@@ -112,6 +112,25 @@ def test_prefix_property_and_offset_linearity():
     assert (full - full2) % (1 << n) == (dv - dv2) % (1 << n)
 
 
+@pytest.mark.parametrize("batch", [1, 300])
+def test_unaligned_shift_across_tiles(batch):
+    # (n - r) % 32 != 0 with outputs spanning many carry tiles, in both the
+    # look-back (few blocks) and the sequential (many blocks) carry modes
+    n = 300_007 if batch > 1 else 3_000_013
+    rng = np.random.default_rng(21 + batch)
+    nb = (n + 7) // 8
+    arr = rng.integers(0, 256, size=(3, batch, nb), dtype=np.uint8)
+    arr[:, :, -1] &= (1 << (n % 8)) - 1
+    arr[1, :, 0] |= 1
+    dx, dc, dd = (torch.from_numpy(a).cuda() for a in arr)
+    for r in (n - 1, n // 2 + 3, 4097 * 32 + 5):
+        out = HashEngine(n, r, max_batch=batch).hash_device(dx, dc, dd).cpu().numpy()
+        for i in sorted({0, batch // 2, batch - 1}):
+            want = oracle.compress(arr[0, i].tobytes(), arr[1, i].tobytes(), arr[2, i].tobytes(),
+                                   n, r)
+            assert out[i].tobytes() == want, (batch, r, i)
+
+
 def test_max_size_and_range_errors():
     n = 1 << 27
     rng = random.Random(9)
