@@ -8,7 +8,9 @@ namespace pab {
 
 typedef void (*ConvKernel)(ConvJob, PlanTables, int);
 struct ConvKernels {
-  ConvKernel row, row_small, col_fwd, col_inv;
+  ConvKernel row, row_small;
+  ConvKernel col_fwd, col_inv;      // column passes with lgC == LG (lg even)
+  ConvKernel col_fwd1, col_inv1;    // column passes with lgC == LG + 1 (lg odd)
 };
 
 __device__ __forceinline__ int brev(int x, int bits) {
@@ -78,14 +80,24 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
           v[0][k] = ra[k << SLO0];
           v[1][k] = rx[k << SLO0];
         }
-        const u32 k1 = (u32)brev(q, lgR);
-        u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
-        const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+        if (tab.tw4) {  // precomputed Shoup twiddles (coalesced, L2-resident)
+          const uint2* tp = tab.tw4 + (long long)(P * 2 + 0) * L + ((long long)q << LGC) + o;
 #pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          v[0][k] = mont<P>(v[0][k], m);
-          v[1][k] = mont<P>(v[1][k], m);
-          m = shoup(m, gam, PK<P>::p);
+          for (int k = 0; k < (1 << RS0); ++k) {
+            const uint2 w = __ldg(tp + (k << SLO0));
+            v[0][k] = shoup(v[0][k], w, PK<P>::p);
+            v[1][k] = shoup(v[1][k], w, PK<P>::p);
+          }
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RS0); ++k) {
+            v[0][k] = mont<P>(v[0][k], m);
+            v[1][k] = mont<P>(v[1][k], m);
+            m = shoup(m, gam, PK<P>::p);
+          }
         }
       }
       dif_rt<P, RS0, SLO0, 2>(v, twf + o);
@@ -219,14 +231,21 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             gA[gi] = red(shoup(v[k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
         }
       } else {
-        const u32 k1 = (u32)brev(q, lgR);
-        u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
-        const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
         u32* rx = gX + ((long long)q << LGC) + o;
+        if (tab.tw4) {
+          const uint2* tp = tab.tw4 + (long long)(P * 2 + 1) * L + ((long long)q << LGC) + o;
 #pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
-          m = shoup(m, gam, PK<P>::p);
+          for (int k = 0; k < (1 << RS0); ++k)
+            rx[k << SLO0] = shoup(v[k], __ldg(tp + (k << SLO0)), PK<P>::p);
+        } else {
+          const u32 k1 = (u32)brev(q, lgR);
+          u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+#pragma unroll
+          for (int k = 0; k < (1 << RS0); ++k) {
+            rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
+            m = shoup(m, gam, PK<P>::p);
+          }
         }
       }
     }
@@ -247,14 +266,14 @@ __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int ln
 // smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
 // broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
 // scaled residues.
-template <int P, int LGR>
+template <int P, int LGR, int LGC>
 __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int CT = 1 << lct;
   const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
-  const int lgC = job.lgC;
+  constexpr int lgC = LGC;
   const long long L = 1ll << job.lg;
   const int c0 = blockIdx.x << lct;
   const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
@@ -285,12 +304,21 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
       const int col = c0 + t;
       u32 v[1][1 << RS0];
       if (half) {
+        const int g0 = (o << lgC) + col;
+        constexpr int kTop = ((1 << (RS0 - 1)) - 1) << (SLO0 + lgC);
+        if (g0 + kTop < ilast) {  // every word of the task is valid and unmasked
+          const u32* sp = src + g0;
 #pragma unroll
-        for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
-          const int gi = ((o + (k << SLO0)) << lgC) + col;
-          u32 w = gi < lim ? __ldg(src + gi) : 0u;
-          w &= gi == ilast ? mask : 0xFFFFFFFFu;
-          v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+          for (int k = 0; k < (1 << (RS0 - 1)); ++k)
+            v[0][k] = shoup(__ldg(sp + (k << (SLO0 + lgC))), 1u, PK<P>::one_sh, PK<P>::p);
+        } else {
+#pragma unroll
+          for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
+            const int gi = g0 + (k << (SLO0 + lgC));
+            u32 w = gi < lim ? __ldg(src + gi) : 0u;
+            w &= gi == ilast ? mask : 0xFFFFFFFFu;
+            v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+          }
         }
         dif_rt_half<P, RS0, SLO0>(v, twf + o);
       } else {
@@ -337,14 +365,14 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
   }
 }
 
-template <int P, int LGR>
+template <int P, int LGR, int LGC>
 __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int CT = 1 << lct;
   const int b = blockIdx.z;
-  const int lgC = job.lgC;
+  constexpr int lgC = LGC;
   const long long L = 1ll << job.lg;
   const int c0 = blockIdx.x << lct;
   const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
@@ -421,20 +449,20 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
   }
 }
 
-template <int LGR>
+template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
-    case 0: col_fwd_body<0, LGR>(job, tab, lct); break;
-    case 1: col_fwd_body<1, LGR>(job, tab, lct); break;
-    default: col_fwd_body<2, LGR>(job, tab, lct); break;
+    case 0: col_fwd_body<0, LGR, LGC>(job, tab, lct); break;
+    case 1: col_fwd_body<1, LGR, LGC>(job, tab, lct); break;
+    default: col_fwd_body<2, LGR, LGC>(job, tab, lct); break;
   }
 }
-template <int LGR>
+template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
-    case 0: col_inv_body<0, LGR>(job, tab, lct); break;
-    case 1: col_inv_body<1, LGR>(job, tab, lct); break;
-    default: col_inv_body<2, LGR>(job, tab, lct); break;
+    case 0: col_inv_body<0, LGR, LGC>(job, tab, lct); break;
+    case 1: col_inv_body<1, LGR, LGC>(job, tab, lct); break;
+    default: col_inv_body<2, LGR, LGC>(job, tab, lct); break;
   }
 }
 
@@ -448,8 +476,12 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
     ConvKernels k;                                                                   \
     k.row = k_row<LG, false>;                                                        \
     k.row_small = k_row<LG, true>;                                                   \
-    k.col_fwd = (LG >= 6) ? (ConvKernel)k_col_fwd<(LG >= 6 ? LG : 6)> : nullptr;     \
-    k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<(LG >= 6 ? LG : 6)> : nullptr;     \
+    constexpr int R_ = LG >= 6 ? LG : 6;                                             \
+    constexpr int C1_ = R_ + 1 <= 12 ? R_ + 1 : 12;                                   \
+    k.col_fwd = (LG >= 6) ? (ConvKernel)k_col_fwd<R_, R_> : nullptr;                  \
+    k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<R_, R_> : nullptr;                  \
+    k.col_fwd1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd<R_, C1_> : nullptr;     \
+    k.col_inv1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_inv<R_, C1_> : nullptr;     \
     return k;                                                                        \
   }                                                                                  \
   }

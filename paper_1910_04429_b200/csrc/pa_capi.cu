@@ -30,6 +30,7 @@ using namespace pab;
 namespace {
 
 thread_local std::string g_err;
+constexpr int kTw4MaxLg = 18;  // full four-step twiddle tables up to L = 2^18 (12 MiB, L2-resident)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -87,6 +88,7 @@ struct Plan {
   u32* tlo_m = nullptr;
   uint2* thi = nullptr;
   uint2* g = nullptr;
+  uint2* tw4 = nullptr;
   u32 scale[kNumPrimes], scale_sh[kNumPrimes];
 };
 
@@ -234,6 +236,32 @@ int get_plan(DevState* ds, int lg, const Plan** out) {
      "upload plan tables");
   CK(cudaMemcpy(pl.thi, thi.data(), thi.size() * sizeof(uint2), cudaMemcpyHostToDevice),
      "upload plan tables");
+  // full four-step twiddle tables for small L (<= 2^kTw4MaxLg): 48 L bytes, L2-resident
+  if (pl.lgR > 0 && lg <= kTw4MaxLg) {
+    const size_t L = (size_t)1 << lg;
+    const int C = 1 << pl.lgC, R = 1 << pl.lgR;
+    std::vector<uint2> t4((size_t)kNumPrimes * 2 * L);
+    for (int i = 0; i < kNumPrimes; ++i) {
+      const u32 p = kPrimes[i];
+      for (int dir = 0; dir < 2; ++dir) {
+        const u32 wL = root_pow2(i, lg, dir);
+        uint2* t = &t4[((size_t)i * 2 + dir) * L];
+        for (int q = 0; q < R; ++q) {
+          int k1 = 0;  // bit reversal of q in lgR bits
+          for (int b = 0; b < pl.lgR; ++b) k1 |= ((q >> b) & 1) << (pl.lgR - 1 - b);
+          const u64 step = powmod(wL, (u64)k1, p);
+          u64 x = 1;
+          for (int c = 0; c < C; ++c) {
+            t[(size_t)q * C + c] = make_uint2((u32)x, shoup_of((u32)x, p));
+            x = x * step % p;
+          }
+        }
+      }
+    }
+    CK(cudaMalloc(&pl.tw4, t4.size() * sizeof(uint2)), "alloc twiddle tables");
+    CK(cudaMemcpy(pl.tw4, t4.data(), t4.size() * sizeof(uint2), cudaMemcpyHostToDevice),
+       "upload twiddle tables");
+  }
   auto res = ds->plans.emplace(lg, pl);
   *out = &res.first->second;
   return PAB_OK;
@@ -245,6 +273,7 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   t.tlo_m = pl->tlo_m;
   t.thi = pl->thi;
   t.g = pl->g;
+  t.tw4 = pl->tw4;
   for (int i = 0; i < kNumPrimes; ++i) {
     t.scale[i] = pl->scale[i];
     t.scale_sh[i] = pl->scale_sh[i];
@@ -266,7 +295,8 @@ int lg_for(u64 len) {  // smallest lg with 2^lg >= len, at least 6
   return lg;
 }
 
-constexpr u64 kMaxChunk = 16384;  // blocks per launch (grid.y/z <= 65535)
+constexpr u64 kMaxChunk = 16384;
+  // blocks per launch (grid.y/z <= 65535)
 
 u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 u64 round_up(u64 a, u64 b) { return ceil_div(a, b) * b; }

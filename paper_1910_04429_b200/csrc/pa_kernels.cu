@@ -488,17 +488,19 @@ static ConvKernels conv_for(int lg) {
     case 10: return conv_kernels_10();
     case 11: return conv_kernels_11();
     case 12: return conv_kernels_12();
-    default: return ConvKernels{nullptr, nullptr, nullptr, nullptr};
+    default: return ConvKernels{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   }
 }
 static ConvKernel row_kernel(int lg, bool small) {
   const ConvKernels k = conv_for(lg);
   return small ? k.row_small : k.row;
 }
-static ConvKernel col_kernel(int lg, bool inv) {
-  if (lg < 6) return nullptr;
-  const ConvKernels k = conv_for(lg);
-  return inv ? k.col_inv : k.col_fwd;
+static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
+  if (lgR < 6) return nullptr;
+  const ConvKernels k = conv_for(lgR);
+  if (lgC == lgR) return inv ? k.col_inv : k.col_fwd;
+  if (lgC == lgR + 1) return inv ? k.col_inv1 : k.col_fwd1;
+  return nullptr;
 }
 
 static int col_lct(int lgR, int lgC) {
@@ -521,7 +523,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smc = (size_t)sm_len(job.lgR) * (1u << lct) * 4;
   {
     prof::Scope ps_("k_col_fwd", st);
-    col_kernel(job.lgR, false)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads,
+    col_kernel(job.lgR, job.lgC, false)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads,
                                  smc, st>>>(job, tab, lct);
   }
   int lnr = 13 - job.lgC;  // 8K words of rows (A+X: 16K words) per CTA
@@ -535,7 +537,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    col_kernel(job.lgR, true)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc,
+    col_kernel(job.lgR, job.lgC, true)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc,
                                 st>>>(job, tab, lct);
   }
 }
@@ -555,8 +557,10 @@ void set_kernel_attrs() {
     for (int s = 0; s < 2; ++s) {
       ConvKernel k = row_kernel(lg, s != 0);
       if (k) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      ConvKernel c = col_kernel(lg, s != 0);
-      if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      for (int dc = 0; dc < 2; ++dc) {
+        ConvKernel c = col_kernel(lg, lg + dc, s != 0);
+        if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }
     }
   }
 }

@@ -13,6 +13,8 @@ struct PlanTables {
   const u32* tlo_m;    // Montgomery form of w_L^e, e < 4096
   const uint2* thi;    // Shoup pairs of w_L^(4096 j)
   const uint2* g;      // Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row-pass twiddle step)
+  const uint2* tw4;    // [3][2][L] full four-step twiddles w_L^(+-c*brev(q)) at [q*C + c],
+                       // Shoup pairs; only for small L (L2-resident), else null
   u32 scale[3];        // L^-1 * 2^32 mod p: undoes the length and the Montgomery factor
   u32 scale_sh[3];     // of the pointwise product (Shoup companions)
 };
