@@ -220,13 +220,21 @@ def time_device(eng, dx, dc, dd, dout, steps, warmup, dist, profile=True):
 
 
 def max_over_ranks(v: float, dist) -> float:
+    """Max of a per-rank timing over all ranks (NCCL on GPUs, gloo on CPU)."""
     if not dist:
         return v
     import torch
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def rank_seeds(cfg_seeds, rank: int) -> list[int]:
+    """Weak scaling: rank k hashes seeds k*B .. k*B+B-1 (rank 0 = BASELINE's seeds)."""
+    per_rank = len(cfg_seeds)
+    return [rank * per_rank + s for s in cfg_seeds]
 
 
 def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
@@ -243,7 +251,7 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
         dist = tdist
     n, r = cfg["n"], cfg["ms"][0]
     per_rank = len(cfg["seeds"])
-    seeds = [rank * per_rank + s for s in cfg["seeds"]]
+    seeds = rank_seeds(cfg["seeds"], rank)
     xs, cs, ds = workloads.batch_inputs(n, seeds)
     px, pc, pd = (torch.from_numpy(a).pin_memory() for a in (xs, cs, ds))
     dx, dc, dd = (t.cuda() for t in (px, pc, pd))

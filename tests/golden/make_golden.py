@@ -141,7 +141,38 @@ def gen_small() -> dict:
     return {"hash": cases, "mul": prods}
 
 
+def gen_runpa() -> dict:
+    """Key files hashed by the reference's own batch driver (bench.run_pa, bench.py:223-265)."""
+    import tempfile
+
+    from modpa import bench
+
+    rng = random.Random(0x9A)
+    cases = []
+    for n, nblocks, extra, kw, order in [
+        (4096, 3, 0, dict(ratio=0.5), LSF),
+        (64, 5, 3, dict(out_bits=32), LSF),
+        (1024, 4, 0, dict(ratio=0.3), MSF),
+        (100_000, 3, 7, dict(out_bits=33_333), LSF),
+    ]:
+        data = rng.randbytes(nblocks * n // 8 + extra)
+        with tempfile.TemporaryDirectory() as td:
+            inp, out = os.path.join(td, "key.bin"), os.path.join(td, "out.bin")
+            open(inp, "wb").write(data)
+            cfg = bench.RunConfig(sizes=(n,), rng_seed=rng.randrange(1000), in_path=inp,
+                                  out_path=out, order=order, **kw)
+            bench.run_pa(cfg)
+            cases.append({"n": n, "rng_seed": cfg.rng_seed, "order": order.value,
+                          "kw": kw, "data": data.hex(), "out": open(out, "rb").read().hex()})
+    return {"cases": cases}
+
+
 if __name__ == "__main__":
+    if "--runpa-only" in sys.argv:
+        with open(os.path.join(HERE, "runpa.json"), "w") as f:
+            json.dump(gen_runpa(), f, indent=0)
+        print("runpa done")
+        sys.exit(0)
     procs = int(os.environ.get("GOLDEN_PROCS", os.cpu_count() or 1))
     small = gen_small()
     with open(os.path.join(HERE, "small.json"), "w") as f:

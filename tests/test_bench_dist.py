@@ -1,0 +1,49 @@
+"""Multi-rank host logic of bench.py on CPU (gloo, world_size 2): max-over-ranks
+timing and the weak-scaling block-seed assignment (no GPU needed)."""
+import os
+import socket
+
+import torch.multiprocessing as mp
+
+import bench
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = bench.max_over_ranks(1.5 + rank, dist)
+        seeds = bench.rank_seeds(tuple(range(4)), rank)
+        q.put((rank, m, seeds))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_max_over_ranks_and_seed_shards_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(60)
+    res = {r: (m, s) for r, m, s in (q.get(timeout=5) for _ in ps)}
+    assert res[0][0] == res[1][0] == 2.5
+    assert res[0][1] == [0, 1, 2, 3] and res[1][1] == [4, 5, 6, 7]
+
+
+def test_kernel_model_positive():
+    m = bench.kernel_model(10**6, 5 * 10**5, 1024) if os.path.exists(
+        os.path.join(bench.ROOT, "paper_1910_04429_b200", "_lib", "libpa_b200.so")) else None
+    if m:
+        assert set(m) >= {"k_col_fwd", "k_row", "k_col_inv", "k_carry"}
+        assert all(v["bytes"] > 0 for k, v in m.items() if k.startswith("k_"))
