@@ -94,6 +94,9 @@ struct Plan {
 
 struct HostCtx {  // cached buffers for the host-pointer entry points
   cudaStream_t stream = nullptr;
+  uint8_t* mapped = nullptr;      // pinned, device-mapped staging for tiny blocks
+  uint8_t* mapped_dev = nullptr;
+  size_t mapped_bytes = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
   uint8_t* dev_io = nullptr;
@@ -507,6 +510,29 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
   HostCtx& h = ds->host;
   std::lock_guard<std::mutex> lk(h.mu);
   const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  // tiny blocks: one kernel over mapped pinned memory (one launch, one sync)
+  const size_t tiny_io = (size_t)batch * (3 * nbytes + rbytes);
+  if (n_bits <= (u64)kTinyBits && tiny_io <= ((size_t)1 << 20)) {
+    if (!h.stream) CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking), "stream");
+    if (!h.mapped) {
+      h.mapped_bytes = (size_t)1 << 20;
+      CK(cudaHostAlloc((void**)&h.mapped, h.mapped_bytes, cudaHostAllocMapped), "host alloc");
+      CK(cudaHostGetDevicePointer((void**)&h.mapped_dev, h.mapped, 0), "mapped pointer");
+    }
+    std::memcpy(h.mapped, x, batch * nbytes);
+    std::memcpy(h.mapped + batch * nbytes, c, batch * nbytes);
+    std::memcpy(h.mapped + 2 * batch * nbytes, d, batch * nbytes);
+    uint8_t* dout = h.mapped_dev + 3 * batch * nbytes;
+    launch_tiny(h.mapped_dev, h.mapped_dev + batch * nbytes, h.mapped_dev + 2 * batch * nbytes,
+                (long long)nbytes, (int)n_bits, (int)r_bits, byte_order == PAB_ORDER_MSF,
+                (int)batch, dout, (long long)rbytes, h.stream);
+    CK(cudaGetLastError(), "kernel launch");
+    CK(cudaStreamSynchronize(h.stream), "synchronize");
+    std::memcpy(out, h.mapped + 3 * batch * nbytes, batch * rbytes);
+    return PAB_OK;
+  }
   const u64 in_stride = round_up(nbytes, 16), out_stride = round_up(rbytes, 16);
   // at most ~2 GiB of transform workspace per chunk
   u64 chunk = batch;

@@ -466,6 +466,115 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry_seq(ConvJob job) {
   for (int tile = 0; tile < job.tiles; ++tile) c = carry_tile<false>(job, sm, b, tile, c);
 }
 
+
+// ---------------------------------------------------------------------------
+// Tiny blocks (n <= kTinyBits): one warp per block, low-half schoolbook product
+// with 96-bit column sums, + d, sequential carry (<= 64 words), mask, shift,
+// serialize.  Used by the host path with mapped pinned memory so a drop-in
+// compress() call is one launch + one synchronize (the reference's desk-scale
+// tests call compress ~1.6M times at alpha <= 10, pkg/tests/test_acceptance.py:96-128).
+__global__ void __launch_bounds__(32) k_tiny(const uint8_t* __restrict__ x,
+                                             const uint8_t* __restrict__ c,
+                                             const uint8_t* __restrict__ d, long long stride,
+                                             int n_bits, int r_bits, int msf,
+                                             uint8_t* __restrict__ out, long long out_stride) {
+  constexpr int KW = kTinyBits / 32;
+  __shared__ u32 sx[KW], sc[KW], sd[KW], st[KW + 1];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const int nbytes = (n_bits + 7) >> 3, K = (n_bits + 31) >> 5;
+  const uint8_t* px = x + (long long)b * stride;
+  const uint8_t* pc = c + (long long)b * stride;
+  const uint8_t* pd = d + (long long)b * stride;
+  for (int j = lane; j < KW; j += 32) {
+    u32 wx = 0, wc = 0, wd = 0;
+    if (j < K) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int bi = 4 * j + q;
+        if (bi < nbytes) {
+          const int src = msf ? nbytes - 1 - bi : bi;
+          wx |= (u32)px[src] << (8 * q);
+          wc |= (u32)pc[src] << (8 * q);
+          wd |= (u32)pd[src] << (8 * q);
+        }
+      }
+      if (j == K - 1 && (n_bits & 31)) {
+        const u32 m = (1u << (n_bits & 31)) - 1u;
+        wx &= m;
+        wc &= m;
+        wd &= m;
+      }
+    }
+    sx[j] = wx;
+    sc[j] = wc;
+    sd[j] = wd;
+  }
+  __syncwarp();
+  // column sums S_k = sum_{i<=k} c_i x_{k-i} + d_k as (lo64, hi32)
+  u64 slo[2];
+  u32 shi[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = lane + 32 * h;
+    u64 lo = 0;
+    u32 hi = 0;
+    if (k < K) {
+      lo = sd[k];
+      for (int i = 0; i <= k; ++i) {
+        const u64 p = (u64)sc[i] * sx[k - i];
+        lo += p;
+        hi += (lo < p) ? 1u : 0u;
+      }
+    }
+    slo[h] = lo;
+    shi[h] = hi;
+  }
+  // sequential carry by lane 0 over K words (carry < 2^38)
+  __shared__ u64 s_lo[KW];
+  __shared__ u32 s_hi[KW];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = lane + 32 * h;
+    if (k < KW) {
+      s_lo[k] = slo[h];
+      s_hi[k] = shi[h];
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    u64 carry = 0;  // < 2^39
+    for (int k = 0; k < K; ++k) {
+      const u64 lo = s_lo[k];
+      const u64 t = (lo & 0xFFFFFFFFull) + (carry & 0xFFFFFFFFull);
+      st[k] = (u32)t;
+      carry = (t >> 32) + (lo >> 32) + (carry >> 32) + ((u64)s_hi[k] << 32);
+    }
+    if (n_bits & 31) st[K - 1] &= (1u << (n_bits & 31)) - 1u;
+    st[K] = 0u;
+  }
+  __syncwarp();
+  // y = T >> (n - r): ceil(r/8) bytes
+  const int rb = (r_bits + 7) >> 3, shift = n_bits - r_bits;
+  uint8_t* po = out + (long long)b * out_stride;
+  for (int q = lane; q < rb; q += 32) {
+    const int bit = shift + 8 * q;
+    const int w = bit >> 5, o = bit & 31;
+    u32 v = st[w] >> o;
+    if (o > 24 && w + 1 <= K) v |= st[w + 1] << (32 - o);
+    u32 byte = v & 0xFFu;
+    const int valid = r_bits - 8 * q;  // bits of y in this byte
+    if (valid < 8) byte &= (1u << valid) - 1u;
+    po[msf ? rb - 1 - q : q] = (uint8_t)byte;
+  }
+}
+
+void launch_tiny(const uint8_t* x, const uint8_t* c, const uint8_t* d, long long stride, int n_bits,
+                 int r_bits, int msf, int batch, uint8_t* out, long long out_stride,
+                 cudaStream_t st) {
+  prof::Scope ps_("k_tiny", st);
+  k_tiny<<<batch, 32, 0, st>>>(x, c, d, stride, n_bits, r_bits, msf, out, out_stride);
+}
+
 // ---------------------------------------------------------------------------
 // dispatch over compile-time transform sizes
 

@@ -106,7 +106,7 @@ def gpu_hasher(batch: int = 256) -> Hasher:
         eng = HashEngine(n, r, max_batch=min(batch, max(1, x.shape[0])),
                          order=_native.ORDER_MSF if order is WordOrder.MOST_SIGNIFICANT_FIRST
                          else _native.ORDER_LSF)
-        px, pc, pd = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (x, c, d))
+        px, pc, pd = (torch.from_numpy(np.array(a, copy=True)).pin_memory() for a in (x, c, d))
         out = eng.hash_host(px, pc, pd, streams=3)
         torch.cuda.synchronize()
         return out.numpy()
