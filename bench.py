@@ -94,8 +94,8 @@ class ClockSampler:
 def plan_geometry(n: int) -> dict:
     from paper_1910_04429_b200 import _native
 
-    lg, lr, lc = _native.plan_info(n)
-    return {"lg": lg, "lgR": lr, "lgC": lc, "L": 1 << lg, "K": (n + 31) // 32}
+    m, lg, lr, lc = _native.plan_info(n)
+    return {"m": m, "lg": lg, "lgR": lr, "lgC": lc, "L": m << lg, "K": (n + 31) // 32}
 
 
 def kernel_model(n: int, r: int, blocks: int) -> dict:
@@ -107,9 +107,10 @@ def kernel_model(n: int, r: int, blocks: int) -> dict:
     four-step twiddle application.
     """
     g = plan_geometry(n)
-    L, K, lgR, lgC = g["L"], g["K"], g["lgR"], g["lgC"]
+    L, K, lgR, lgC, mr = g["L"], g["K"], g["lgR"], g["lgC"], g["m"]
     nb, rb, mw = (n + 7) // 8, (r + 7) // 8, (r + 31) // 32
     P = 3
+    rad = {1: 0, 3: 25, 5: 56}[mr]  # ops per radix-m group (incl. its twiddles)
     bf = lambda lg: (L // 2) * lg  # butterflies of one length-L transform restricted to lg stages
     m = {}
     m["k_pack"] = dict(bytes=blocks * 3 * (nb + 4 * K), ops=0)
@@ -120,11 +121,11 @@ def kernel_model(n: int, r: int, blocks: int) -> dict:
                                  ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 2 * L * 3))
     else:
         m["k_col_fwd"] = dict(bytes=blocks * 2 * (4 * K + P * 4 * L),
-                              ops=blocks * 2 * P * (bf(lgR) * 7 + L * 3))
+                              ops=blocks * 2 * P * (bf(lgR) * 7 + L * 3 + (L // mr) * rad))
         m["k_row"] = dict(bytes=blocks * P * 3 * 4 * L,
                           ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 3 * L * 8))
         m["k_col_inv"] = dict(bytes=blocks * P * (4 * L + 4 * K),
-                              ops=blocks * P * (bf(lgR) * 7 + L * 4))
+                              ops=blocks * P * (bf(lgR) * 7 + L * 4 + (L // mr) * rad))
     return m
 
 

@@ -48,8 +48,13 @@ const char* pab_last_error(void);
 /* Largest block size n (bits) the exact three-prime convolution supports. */
 uint64_t pab_max_bits(void);
 
-/* Transform geometry chosen for an n-bit hash: L = 2^lg = 2^lgR * 2^lgC. */
-int pab_plan_info(uint64_t n_bits, int* lg, int* lg_rows, int* lg_cols);
+/*
+ * Transform geometry chosen for an n-bit hash: length L = radix * 2^lg (radix
+ * 1, 3 or 5), split into columns of R = radix * 2^lg_rows rows and rows of
+ * C = 2^lg_cols (lg_rows == 0: one CTA per block and prime).  Any pointer may
+ * be NULL.
+ */
+int pab_plan_info(uint64_t n_bits, int* radix, int* lg, int* lg_rows, int* lg_cols);
 
 /*
  * Device workspace needed to hash `batch` n-bit blocks in one pass.

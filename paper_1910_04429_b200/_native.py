@@ -31,8 +31,7 @@ SIGNATURES = {
     "pab_version": (ctypes.c_int, []),
     "pab_last_error": (ctypes.c_char_p, []),
     "pab_max_bits": (ctypes.c_uint64, []),
-    "pab_plan_info": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_int),
-                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "pab_plan_info": (ctypes.c_int, [ctypes.c_uint64] + [ctypes.POINTER(ctypes.c_int)] * 4),
     "pab_hash_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
     "pab_hash_batch": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _u8p,
@@ -113,11 +112,13 @@ def mul_host(a: bytes, b: bytes, device: int | None = None) -> bytes:
     return out.raw
 
 
-def plan_info(n: int) -> tuple[int, int, int]:
+def plan_info(n: int) -> tuple[int, int, int, int]:
+    """(radix m, lg, lg_rows, lg_cols): L = m * 2^lg, R = m * 2^lg_rows, C = 2^lg_cols."""
     lib = load()
-    lg, lr, lc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    check(lib.pab_plan_info(n, ctypes.byref(lg), ctypes.byref(lr), ctypes.byref(lc)))
-    return lg.value, lr.value, lc.value
+    m, lg, lr, lc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    check(lib.pab_plan_info(n, ctypes.byref(m), ctypes.byref(lg), ctypes.byref(lr),
+                            ctypes.byref(lc)))
+    return m.value, lg.value, lr.value, lc.value
 
 
 def profile_enable(on: bool = True) -> None:

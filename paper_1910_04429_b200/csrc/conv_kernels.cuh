@@ -11,6 +11,7 @@ struct ConvKernels {
   ConvKernel row, row_small;
   ConvKernel col_fwd, col_inv;      // column passes with lgC == LG (lg even)
   ConvKernel col_fwd1, col_inv1;    // column passes with lgC == LG + 1 (lg odd)
+  ConvKernel colm_fwd[2], colm_inv[2];  // mixed radix M = 3, 5 with LGR2 == LG (lgC runtime)
 };
 
 __device__ __forceinline__ int brev(int x, int bits) {
@@ -28,10 +29,15 @@ __device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long
 // four-step twiddle seed w_L^e * 2^32 (Montgomery form, lazy [0, 2p)), e < L
 template <int P>
 __device__ __forceinline__ u32 tw_seed(const PlanTables& tab, int dir, u32 e) {
-  const int off = (P * 2 + dir) * kTwN;
-  const u32 lo = __ldg(&tab.tlo_m[off + (e & (kTwN - 1))]);
-  const uint2 hi = __ldg(&tab.thi[off + (e >> kTwLg)]);
+  const u32 lo = __ldg(&tab.tlo_m[(P * 2 + dir) * kTwN + (e & (kTwN - 1))]);
+  const uint2 hi = __ldg(&tab.thi[(P * 2 + dir) * tab.thi_stride + (e >> kTwLg)]);
   return shoup(lo, hi, PK<P>::p);
+}
+
+// column frequency of storage row q: the column DFT (radix-m stage, then
+// 2^lgR pow2 DIF) leaves row q = s * 2^lgR + pos holding k1 = s + m * brev(pos)
+__device__ __forceinline__ u32 row_k1(int q, int m, int lgR) {
+  return (u32)((q >> lgR) + m * brev(q & ((1 << lgR) - 1), lgR));
 }
 
 // ---------------------------------------------------------------------------
@@ -49,7 +55,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
   const int b = blockIdx.z;
   const int q0 = blockIdx.x << lnr;
   const int lgR = job.lgR;
-  const long long L = 1ll << job.lg;
+  const long long L = job.L;
   u32* sA = smem;
   u32* sX = smem + NR * T;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
@@ -89,9 +95,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             v[1][k] = shoup(v[1][k], w, PK<P>::p);
           }
         } else {
-          const u32 k1 = (u32)brev(q, lgR);
+          const u32 k1 = row_k1(q, job.m, lgR);
           u32 m = tw_seed<P>(tab, 0, (u32)o * k1);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * tab.tstride + k1]);
 #pragma unroll
           for (int k = 0; k < (1 << RS0); ++k) {
             v[0][k] = mont<P>(v[0][k], m);
@@ -150,9 +156,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             x[0][k] = shoup(fetch_word(wX, k, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
           }
         } else {
-          const u32 k1 = (u32)brev(q, lgR);
+          const u32 k1 = row_k1(q, job.m, lgR);
           u32 m = tw_seed<P>(tab, 0, 0u);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * kTwN + k1]);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 0) * tab.tstride + k1]);
 #pragma unroll
           for (int k = 0; k < (1 << RSL); ++k) {
             a[0][k] = mont<P>(gA[((long long)q << LGC) + k], m);
@@ -180,9 +186,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             if (k < job.nRes)
               gA[k] = red(shoup(x[0][k], tab.scale[P], tab.scale_sh[P], PK<P>::p), PK<P>::p);
         } else {
-          const u32 k1 = (u32)brev(q, lgR);
+          const u32 k1 = row_k1(q, job.m, lgR);
           u32 m = tw_seed<P>(tab, 1, 0u);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * tab.tstride + k1]);
 #pragma unroll
           for (int k = 0; k < (1 << RSL); ++k) {
             gX[((long long)q << LGC) + k] = mont<P>(red(x[0][k], PK<P>::two_p), m);
@@ -238,9 +244,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
           for (int k = 0; k < (1 << RS0); ++k)
             rx[k << SLO0] = shoup(v[k], __ldg(tp + (k << SLO0)), PK<P>::p);
         } else {
-          const u32 k1 = (u32)brev(q, lgR);
+          const u32 k1 = row_k1(q, job.m, lgR);
           u32 m = tw_seed<P>(tab, 1, (u32)o * k1);
-          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * kTwN + k1]);
+          const uint2 gam = __ldg(&tab.g[(P * 2 + 1) * tab.tstride + k1]);
 #pragma unroll
           for (int k = 0; k < (1 << RS0); ++k) {
             rx[k << SLO0] = mont<P>(red(v[k], PK<P>::two_p), m);
@@ -274,7 +280,7 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
   const int CT = 1 << lct;
   const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
   constexpr int lgC = LGC;
-  const long long L = 1ll << job.lg;
+  const long long L = job.L;
   const int c0 = blockIdx.x << lct;
   const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
   const long long kv = op ? job.kX : job.kA;
@@ -373,7 +379,7 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
   const int CT = 1 << lct;
   const int b = blockIdx.z;
   constexpr int lgC = LGC;
-  const long long L = 1ll << job.lg;
+  const long long L = job.L;
   const int c0 = blockIdx.x << lct;
   const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
   u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
@@ -449,6 +455,174 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
   }
 }
 
+// ---------------------------------------------------------------------------
+// Mixed-radix column passes: columns of length R = M * 2^LGR2 (M = 3 or 5).
+// Forward: radix-M stage over rows {j + t*R2} (from the operand words) with
+// twiddles w_R^(j*s) -> M interleaved sub-columns s of length R2 (smem rows
+// s*R2 + j) -> pow2 DIF of each -> buf.  Inverse mirrors it.  lgC is runtime.
+
+// one smem->smem pow2 pass over the M sub-transforms (interleaved layout)
+template <int P, int M, int LGR2, int RS, int SLO, bool DIF>
+__device__ __forceinline__ void colm_pass(u32* smem, int lct, const uint2* __restrict__ tw) {
+  const int CT = 1 << lct;
+  constexpr int T2 = sm_len(LGR2);
+  constexpr int LGG = LGR2 - RS;
+  for (int task = threadIdx.x; task < ((CT * M) << LGG); task += blockDim.x) {
+    const int t = task & (CT - 1), rest = task >> lct;
+    const int g = rest & ((1 << LGG) - 1), s = rest >> LGG;
+    const int o = g & ((1 << SLO) - 1), blk = g >> SLO;
+    const int base = (s * T2 + sm_idx((blk << (SLO + RS)) + o)) * CT + t;
+    u32 v[1][1 << RS];
+#pragma unroll
+    for (int k = 0; k < (1 << RS); ++k) v[0][k] = smem[base + k * sm_step(SLO) * CT];
+    if constexpr (DIF) {
+      if constexpr (SLO == 0) dif_ct<P, RS, 1>(v);
+      else dif_rt<P, RS, SLO, 1>(v, tw + o);
+    } else {
+      if constexpr (SLO == 0) dit_ct<P, RS>(v[0]);
+      else dit_rt<P, RS, SLO>(v[0], tw + o);
+    }
+#pragma unroll
+    for (int k = 0; k < (1 << RS); ++k) smem[base + k * sm_step(SLO) * CT] = v[0][k];
+  }
+}
+
+template <int P, int M, int LGR2>
+__device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR2);
+  constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
+  const int CT = 1 << lct;
+  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
+  const int lgC = job.lgC;
+  const long long L = job.L;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
+  const long long kv = op ? job.kX : job.kA;
+  const u32 mask = op ? job.maskX : job.maskA;
+  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
+  const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
+  const uint2* trad = tab.trad + (P * 2 + 0) * tab.tstride;
+  const int lim = (int)(kv < L ? kv : L), ilast = (int)kv - 1;
+  // radix-M stage straight from the operand words
+  for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
+    const int t = task & (CT - 1), j = task >> lct;
+    u32 a[M];
+#pragma unroll
+    for (int s = 0; s < M; ++s) {
+      const int gi = ((j + s * R2) << lgC) + c0 + t;
+      u32 w = gi < lim ? __ldg(src + gi) : 0u;
+      w &= gi == ilast ? mask : 0xFFFFFFFFu;
+      a[s] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+    }
+    radix_m<P, M, false>(a);
+#pragma unroll
+    for (int s = 1; s < M; ++s) a[s] = shoup(a[s], __ldg(trad + j * s), PK<P>::p);
+#pragma unroll
+    for (int s = 0; s < M; ++s) smem[(s * T2 + sm_idx(j)) * CT + t] = a[s];
+  }
+  __syncthreads();
+  if constexpr (PP.n >= 2) {
+    colm_pass<P, M, LGR2, PP.rs[0], PP.slo[0], true>(smem, lct, twf);
+    __syncthreads();
+  }
+  if constexpr (PP.n == 3) {
+    colm_pass<P, M, LGR2, PP.rs[1], PP.slo[1], true>(smem, lct, twf);
+    __syncthreads();
+  }
+  // last pow2 pass (stages RSL-1..0, compile-time twiddles) -> global rows s*R2 + pos
+  constexpr int RSL = PP.rs[PP.n - 1];
+  constexpr int LGG = LGR2 - RSL;
+  for (int task = threadIdx.x; task < ((CT * M) << LGG); task += blockDim.x) {
+    const int t = task & (CT - 1), rest = task >> lct;
+    const int g = rest & ((1 << LGG) - 1), s = rest >> LGG;
+    const int base = (s * T2 + sm_idx(g << RSL)) * CT + t;
+    u32 v[1][1 << RSL];
+#pragma unroll
+    for (int k = 0; k < (1 << RSL); ++k) v[0][k] = smem[base + k * CT];
+    dif_ct<P, RSL, 1>(v);
+    u32* d = dst + ((long long)(s * R2 + (g << RSL)) << lgC) + c0 + t;
+#pragma unroll
+    for (int k = 0; k < (1 << RSL); ++k) d[(long long)k << lgC] = v[0][k];
+  }
+}
+
+template <int P, int M, int LGR2>
+__device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
+  extern __shared__ u32 smem[];
+  constexpr PassPlan PP = pass_plan(LGR2);
+  constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
+  const int CT = 1 << lct;
+  const int b = blockIdx.z;
+  const int lgC = job.lgC;
+  const long long L = job.L;
+  const int c0 = blockIdx.x << lct;
+  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
+  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
+  const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
+  const uint2* trad = tab.trad + (P * 2 + 1) * tab.tstride;
+  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
+  // first pow2 DIT pass (stages 0..RSL-1) from global
+  constexpr int RSL = PP.rs[PP.n - 1];
+  {
+    constexpr int LGG = LGR2 - RSL;
+    for (int task = threadIdx.x; task < ((CT * M) << LGG); task += blockDim.x) {
+      const int t = task & (CT - 1), rest = task >> lct;
+      const int g = rest & ((1 << LGG) - 1), s = rest >> LGG;
+      const u32* sp = src + ((long long)(s * R2 + (g << RSL)) << lgC) + c0 + t;
+      u32 v[1 << RSL];
+#pragma unroll
+      for (int k = 0; k < (1 << RSL); ++k) v[k] = sp[(long long)k << lgC];
+      dit_ct<P, RSL>(v);
+      const int base = (s * T2 + sm_idx(g << RSL)) * CT + t;
+#pragma unroll
+      for (int k = 0; k < (1 << RSL); ++k) smem[base + k * CT] = v[k];
+    }
+  }
+  __syncthreads();
+  if constexpr (PP.n == 3) {
+    colm_pass<P, M, LGR2, PP.rs[1], PP.slo[1], false>(smem, lct, twi);
+    __syncthreads();
+  }
+  if constexpr (PP.n >= 2) {
+    colm_pass<P, M, LGR2, PP.rs[0], PP.slo[0], false>(smem, lct, twi);
+    __syncthreads();
+  }
+  // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT, scale -> residues
+  const int nres = (int)(job.nRes < L ? job.nRes : L);
+  for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
+    const int t = task & (CT - 1), j = task >> lct;
+    u32 a[M];
+    a[0] = red(smem[sm_idx(j) * CT + t], PK<P>::two_p);
+#pragma unroll
+    for (int s = 1; s < M; ++s)
+      a[s] = shoup(smem[(s * T2 + sm_idx(j)) * CT + t], __ldg(trad + j * s), PK<P>::p);
+    radix_m<P, M, true>(a);
+#pragma unroll
+    for (int s = 0; s < M; ++s) {
+      const int gi = ((j + s * R2) << lgC) + c0 + t;
+      if (gi < nres) res[gi] = red(shoup(a[s], sc, sc_sh, PK<P>::p), PK<P>::p);
+    }
+  }
+}
+
+template <int M, int LGR2>
+__global__ void __launch_bounds__(256) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: colm_fwd_body<0, M, LGR2>(job, tab, lct); break;
+    case 1: colm_fwd_body<1, M, LGR2>(job, tab, lct); break;
+    default: colm_fwd_body<2, M, LGR2>(job, tab, lct); break;
+  }
+}
+template <int M, int LGR2>
+__global__ void __launch_bounds__(256) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
+  switch (blockIdx.y) {
+    case 0: colm_inv_body<0, M, LGR2>(job, tab, lct); break;
+    case 1: colm_inv_body<1, M, LGR2>(job, tab, lct); break;
+    default: colm_inv_body<2, M, LGR2>(job, tab, lct); break;
+  }
+}
+
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
@@ -482,6 +656,12 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
     k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<R_, R_> : nullptr;                  \
     k.col_fwd1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd<R_, C1_> : nullptr;     \
     k.col_inv1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_inv<R_, C1_> : nullptr;     \
+    constexpr int M2_ = LG >= 3 && LG <= 10 ? LG : 3;                                 \
+    const bool mx_ = LG >= 3 && LG <= 10;                                             \
+    k.colm_fwd[0] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_> : nullptr;                   \
+    k.colm_fwd[1] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_> : nullptr;                   \
+    k.colm_inv[0] = mx_ ? (ConvKernel)k_colm_inv<3, M2_> : nullptr;                   \
+    k.colm_inv[1] = mx_ ? (ConvKernel)k_colm_inv<5, M2_> : nullptr;                   \
     return k;                                                                        \
   }                                                                                  \
   }

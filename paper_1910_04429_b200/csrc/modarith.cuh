@@ -16,9 +16,12 @@ typedef uint32_t u32;
 typedef uint64_t u64;
 
 constexpr int kNumPrimes = 3;
-// p_i = k_i * 2^23 + 1, p_i < 2^30 (so 4p < 2^32); product ~ 2^89.35.
-constexpr u32 kPrimes[kNumPrimes] = {998244353u, 897581057u, 880803841u};
-constexpr int kMaxLg = 23;        // 2-adicity common to all three primes
+// p_i < 2^30 (so 4p < 2^32) with 2^22 * 3 * 5 | p_i - 1 (radix-2/3/5 transform
+// lengths); product ~ 2^89.02, so any coefficient K * (2^32-1)^2 with K < 2^25
+// is recovered exactly by CRT.  kGen: a primitive root of each prime.
+constexpr u32 kPrimes[kNumPrimes] = {943718401u, 880803841u, 754974721u};
+constexpr u32 kGen[kNumPrimes] = {7u, 26u, 11u};
+constexpr int kMaxLg = 22;        // 2-adicity common to all three primes
 constexpr int kTwN = 4096;        // largest in-CTA sub-transform
 constexpr int kTwLg = 12;
 

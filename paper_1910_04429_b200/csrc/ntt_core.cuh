@@ -20,10 +20,6 @@
 
 namespace pab {
 
-// primitive 2^23-th roots of unity (and inverses) of kPrimes (generator^((p-1)/2^23))
-constexpr u32 kRoot23[kNumPrimes] = {15311432u, 872686320u, 273508579u};
-constexpr u32 kIRoot23[kNumPrimes] = {469870224u, 354917575u, 109748732u};
-
 __host__ __device__ constexpr u32 cmul(u32 a, u32 b, u32 p) { return (u32)((u64)a * b % p); }
 __host__ __device__ constexpr u32 cpow(u32 a, u64 e, u32 p) {
   u32 r = 1;
@@ -40,9 +36,15 @@ __host__ __device__ constexpr u32 cmont_neg_inv(u32 p) {
   for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
   return 0u - inv;
 }
-// w_{2^lgo}^e (INV: inverse root)
+// w_N^e with w_N = g^((p-1)/N) (INV: w_N^-e); all roots derive from one generator
+__host__ __device__ constexpr u32 croot_n(int P, bool inv, u64 N, u64 e) {
+  const u32 p = kPrimes[P];
+  const u64 x = (u64)(p - 1) / N * (e % N);
+  return cpow(kGen[P], inv ? (u64)(p - 1) - x : x, p);
+}
+// w_{2^lgo}^e
 __host__ __device__ constexpr u32 croot(int P, bool inv, int lgo, u64 e) {
-  return cpow(inv ? kIRoot23[P] : kRoot23[P], e << (23 - lgo), kPrimes[P]);
+  return croot_n(P, inv, (u64)1 << lgo, e);
 }
 
 template <int P>
@@ -267,6 +269,63 @@ __device__ __forceinline__ void dit_rt_half(u32 (&v)[1 << RS], const uint2* __re
     const u32 a = red(v[k], PK<P>::two_p);
     v[k] = a + (v[k + H] * w.x - __umulhi(v[k + H], w.y) * PK<P>::p);
   });
+}
+
+// ------------------------------------------------------------ radix 3 / 5
+// Length-M DFT of a[0..M) in place (INV: inverse roots), inputs in [0, 2p),
+// outputs in [0, 2p).  Radix-3: y1,2 = a0 - s/2 +- c (a1 - a2), c = (w - w^2)/2.
+// Radix-5: with u_k = a_k + a_{5-k}, v_k = a_k - a_{5-k}, C_k = (w^k + w^-k)/2,
+// S_k = (w^k - w^-k)/2:  y1,4 = a0 + C1 u1 + C2 u2 +- (S1 v1 + S2 v2),
+// y2,3 = a0 + C2 u1 + C1 u2 +- (S2 v1 - S1 v2).  Every product is a Shoup
+// multiply by a compile-time constant.
+template <int P, bool INV>
+__device__ __forceinline__ void radix3(u32 (&a)[3]) {
+  constexpr u32 p = kPrimes[P], tp = 2u * kPrimes[P];
+  constexpr u32 h = (p + 1u) / 2u;  // 1/2
+  constexpr u32 w1 = croot_n(P, INV, 3, 1), w2 = croot_n(P, INV, 3, 2);
+  constexpr u32 c = cmul((w1 + p - w2) % p, h, p);
+  constexpr u32 hs = cshoup(h, p), cs = cshoup(c, p);
+  const u32 s = red(a[1] + a[2], tp);
+  const u32 d = a[1] - a[2] + tp;
+  const u32 y0 = red(a[0] + s, tp);
+  const u32 t1 = s * h - __umulhi(s, hs) * p;
+  const u32 t2 = d * c - __umulhi(d, cs) * p;
+  const u32 u = red(a[0] - t1 + tp, tp);
+  a[0] = y0;
+  a[1] = red(u + t2, tp);
+  a[2] = red(u - t2 + tp, tp);
+}
+
+template <int P, bool INV>
+__device__ __forceinline__ void radix5(u32 (&a)[5]) {
+  constexpr u32 p = kPrimes[P], tp = 2u * kPrimes[P];
+  constexpr u32 h = (p + 1u) / 2u;
+  constexpr u32 w1 = croot_n(P, INV, 5, 1), w2 = croot_n(P, INV, 5, 2);
+  constexpr u32 w3 = croot_n(P, INV, 5, 3), w4 = croot_n(P, INV, 5, 4);
+  constexpr u32 C1 = cmul((w1 + w4) % p, h, p), C2 = cmul((w2 + w3) % p, h, p);
+  constexpr u32 S1 = cmul((w1 + p - w4) % p, h, p), S2 = cmul((w2 + p - w3) % p, h, p);
+  constexpr u32 C1s = cshoup(C1, p), C2s = cshoup(C2, p), S1s = cshoup(S1, p),
+                S2s = cshoup(S2, p);
+  const u32 u1 = a[1] + a[4], v1 = a[1] - a[4] + tp;  // < 4p
+  const u32 u2 = a[2] + a[3], v2 = a[2] - a[3] + tp;
+  const u32 y0 = red(a[0] + red(red(u1, tp) + red(u2, tp), tp), tp);
+  const u32 t1 = red((u1 * C1 - __umulhi(u1, C1s) * p) + (u2 * C2 - __umulhi(u2, C2s) * p), tp);
+  const u32 t2 = red((u1 * C2 - __umulhi(u1, C2s) * p) + (u2 * C1 - __umulhi(u2, C1s) * p), tp);
+  const u32 s1 = red((v1 * S1 - __umulhi(v1, S1s) * p) + (v2 * S2 - __umulhi(v2, S2s) * p), tp);
+  const u32 s2 = red((v1 * S2 - __umulhi(v1, S2s) * p) - (v2 * S1 - __umulhi(v2, S1s) * p) + tp,
+                     tp);
+  const u32 b1 = red(a[0] + t1, tp), b2 = red(a[0] + t2, tp);
+  a[0] = y0;
+  a[1] = red(b1 + s1, tp);
+  a[4] = red(b1 - s1 + tp, tp);
+  a[2] = red(b2 + s2, tp);
+  a[3] = red(b2 - s2 + tp, tp);
+}
+
+template <int P, int M, bool INV>
+__device__ __forceinline__ void radix_m(u32 (&a)[M]) {
+  if constexpr (M == 3) radix3<P, INV>(a);
+  else if constexpr (M == 5) radix5<P, INV>(a);
 }
 
 }  // namespace pab

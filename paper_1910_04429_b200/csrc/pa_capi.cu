@@ -8,6 +8,7 @@
 // three-prime word convolution and its four-step split L = R * C.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -74,20 +75,77 @@ PrimeInfo prime_info(u32 p) {
   return pi;
 }
 
-// root of unity of order 2^k (dir 1: its inverse); the same roots the device
-// code derives at compile time (ntt_core.cuh: croot)
-u32 root_pow2(int prime, int k, int dir) {
+// w_N = g^((p-1)/N) (dir 1: its inverse): the same roots the device code
+// derives at compile time (ntt_core.cuh: croot_n)
+u32 root_of(int prime, u64 N, int dir) {
   const u32 p = kPrimes[prime];
-  const u32 w23 = dir ? kIRoot23[prime] : kRoot23[prime];
-  return (u32)powmod(w23, (u64)1 << (kMaxLg - k), p);
+  const u64 w = powmod(kGen[prime], (u64)(p - 1) / N, p);
+  return dir ? inv_mod((u32)w, p) : (u32)w;
+}
+u32 root_pow2(int prime, int k, int dir) { return root_of(prime, (u64)1 << k, dir); }
+
+// Transform geometry: L = m * 2^lg, columns of R = m * 2^lgR rows, rows of C = 2^lgC.
+// lgR == 0 (m == 1) is the single-CTA path (L <= 4096).
+struct Geo {
+  int m = 1, lg = 0, lgR = 0, lgC = 0;
+  u64 L = 0;
+};
+
+// Cheapest length >= need among m * 2^lg, m in {1, 3, 5} (radix-3/5 column
+// stage costs ~2.5 / ~3.7 radix-2 stages).  Returns false if none fits.
+bool choose_geo(u64 need, Geo* out) {
+  Geo best;
+  double best_cost = 0;
+  bool found = false;
+  const int ms[3] = {1, 3, 5};
+  const double extra[3] = {0.0, 2.5, 3.7};
+  for (int i = 0; i < 3; ++i) {
+    const int m = ms[i];
+    int lg = 0;
+    while (((u64)m << lg) < need || ((u64)m << lg) < 64) ++lg;
+    if (lg > kMaxLg) continue;
+    Geo g;
+    g.m = m;
+    g.lg = lg;
+    g.L = (u64)m << lg;
+    if (m == 1) {
+      if (lg <= kTwLg) {
+        g.lgR = 0;
+        g.lgC = lg;
+      } else {
+        g.lgR = lg / 2;
+        g.lgC = lg - lg / 2;
+      }
+    } else {
+      if (g.L <= (u64)kTwN) continue;  // small lengths: single-CTA pow2 path
+      const double lgm = m == 3 ? 1.585 : 2.322;
+      int lgC = (int)std::ceil((lg + lgm) / 2.0);  // rows >= columns: smaller column panels
+      if (lgC > kTwLg) lgC = kTwLg;
+      if (lgC < 6) lgC = 6;
+      g.lgC = lgC;
+      g.lgR = lg - lgC;
+    }
+    if (!conv_supported(g.m, g.lgR, g.lgC)) continue;
+    const double cost = (double)g.L * (lg + extra[i]);
+    if (!found || cost < best_cost) {
+      best = g;
+      best_cost = cost;
+      found = true;
+    }
+  }
+  if (found) *out = best;
+  return found;
 }
 
 // ------------------------------------------------------------ device state
 struct Plan {
-  int lg, lgR, lgC;
+  Geo geo;
   u32* tlo_m = nullptr;
   uint2* thi = nullptr;
+  int thi_stride = 0;
   uint2* g = nullptr;
+  uint2* trad = nullptr;
+  int tstride = 0;
   uint2* tw4 = nullptr;
   u32 scale[kNumPrimes], scale_sh[kNumPrimes];
 };
@@ -107,7 +165,7 @@ struct HostCtx {  // cached buffers for the host-pointer entry points
 struct DevState {
   bool ready = false;
   uint2* stw = nullptr;
-  std::map<int, Plan> plans;
+  std::map<int, Plan> plans;  // keyed by m * 64 + lg
   HostCtx host;
 };
 
@@ -120,11 +178,14 @@ int ensure_device(int dev, DevState** out) {
   if (!slot) slot.reset(new DevState());
   DevState* ds = slot.get();
   if (!ds->ready) {
-    for (int i = 0; i < kNumPrimes; ++i) {  // the compiled-in roots must be primitive 2^23-th
+    for (int i = 0; i < kNumPrimes; ++i) {  // compiled-in generators must be primitive roots
       const u32 p = kPrimes[i];
-      if (powmod(kRoot23[i], (u64)1 << (kMaxLg - 1), p) != p - 1 ||
-          (u64)kRoot23[i] * kIRoot23[i] % p != 1)
-        return fail(PAB_ECUDA, "internal: bad root-of-unity constants");
+      const u32 q[4] = {2, 3, 5, 0};
+      for (int j = 0; q[j]; ++j)
+        if ((p - 1) % q[j] != 0 || powmod(kGen[i], (p - 1) / q[j], p) == 1)
+          return fail(PAB_ECUDA, "internal: bad prime / generator constants");
+      if (((p - 1) >> kMaxLg) << kMaxLg != p - 1)
+        return fail(PAB_ECUDA, "internal: prime 2-adicity below kMaxLg");
     }
     PrimeInfo pis[kNumPrimes];
     for (int i = 0; i < kNumPrimes; ++i) pis[i] = prime_info(kPrimes[i]);
@@ -176,82 +237,87 @@ int current_device(DevState** ds) {
   return ensure_device(dev, ds);
 }
 
-void split_lg(int lg, int* lgR, int* lgC) {
-  if (lg <= kTwLg) {
-    *lgR = 0;
-    *lgC = lg;
-  } else {
-    *lgR = lg / 2;
-    *lgC = lg - lg / 2;
-  }
+int bitrev(int x, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((x >> b) & 1) << (bits - 1 - b);
+  return r;
 }
 
-int get_plan(DevState* ds, int lg, const Plan** out) {
+int upload(void** dst, const void* src, size_t bytes) {
+  CK(cudaMalloc(dst, bytes), "alloc plan tables");
+  CK(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "upload plan tables");
+  return PAB_OK;
+}
+
+int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = ds->plans.find(lg);
+  const int key = geo.m * 64 + geo.lg;
+  auto it = ds->plans.find(key);
   if (it != ds->plans.end()) {
     *out = &it->second;
     return PAB_OK;
   }
   Plan pl;
-  pl.lg = lg;
-  split_lg(lg, &pl.lgR, &pl.lgC);
+  pl.geo = geo;
+  const u64 L = geo.L;
+  const int R = geo.m << geo.lgR, C = 1 << geo.lgC;
+  pl.thi_stride = (int)((L + kTwN - 1) / kTwN);
+  pl.tstride = R;
   std::vector<u32> tlo((size_t)kNumPrimes * 2 * kTwN, 0);
-  std::vector<uint2> thi((size_t)kNumPrimes * 2 * kTwN, make_uint2(0, 0));
-  std::vector<uint2> gt((size_t)kNumPrimes * 2 * kTwN, make_uint2(0, 0));
+  std::vector<uint2> thi((size_t)kNumPrimes * 2 * pl.thi_stride, make_uint2(0, 0));
+  std::vector<uint2> gt((size_t)kNumPrimes * 2 * R, make_uint2(0, 0));
+  std::vector<uint2> trad((size_t)kNumPrimes * 2 * R, make_uint2(0, 0));
   // row-pass twiddle step: w_L^(k1 * 2^slo0), slo0 = lowest stage of the row's top pass
-  const int slo0 = pass_plan(pl.lgC).slo[0];
+  const int slo0 = pass_plan(geo.lgC).slo[0];
   for (int i = 0; i < kNumPrimes; ++i) {
     const u32 p = kPrimes[i];
     const u64 r32 = ((u64)1 << 32) % p;
     for (int dir = 0; dir < 2; ++dir) {
-      const u32 wL = root_pow2(i, lg, dir);
-      if (pl.lgR > 0) {
+      const size_t pd = (size_t)i * 2 + dir;
+      const u32 wL = root_of(i, L, dir);
+      if (R > 1) {
         const u64 gstep = powmod(wL, (u64)1 << slo0, p);
-        u64 y = 1;
-        for (int k = 0; k < (1 << pl.lgR); ++k) {
-          gt[((size_t)i * 2 + dir) * kTwN + k] = make_uint2((u32)y, shoup_of((u32)y, p));
+        const u64 wR = root_of(i, (u64)R, dir);
+        u64 y = 1, z = 1;
+        for (int k = 0; k < R; ++k) {
+          gt[pd * R + k] = make_uint2((u32)y, shoup_of((u32)y, p));
+          trad[pd * R + k] = make_uint2((u32)z, shoup_of((u32)z, p));
           y = y * gstep % p;
+          z = z * wR % p;
         }
       }
       u64 x = 1;
       for (int e = 0; e < kTwN; ++e) {
-        tlo[((size_t)i * 2 + dir) * kTwN + e] = (u32)(x * r32 % p);
+        tlo[pd * kTwN + e] = (u32)(x * r32 % p);
         x = x * wL % p;
       }
       const u64 step = powmod(wL, kTwN, p);
       x = 1;
-      for (int j = 0; j < kTwN; ++j) {
-        thi[((size_t)i * 2 + dir) * kTwN + j] = make_uint2((u32)x, shoup_of((u32)x, p));
+      for (int j = 0; j < pl.thi_stride; ++j) {
+        thi[pd * pl.thi_stride + j] = make_uint2((u32)x, shoup_of((u32)x, p));
         x = x * step % p;
       }
     }
-    const u64 linv = inv_mod((u32)(((u64)1 << lg) % p), p);
+    const u64 linv = inv_mod((u32)(L % p), p);
     pl.scale[i] = (u32)(linv * r32 % p);
     pl.scale_sh[i] = shoup_of(pl.scale[i], p);
   }
-  CK(cudaMalloc(&pl.tlo_m, tlo.size() * sizeof(u32)), "alloc plan tables");
-  CK(cudaMalloc(&pl.thi, thi.size() * sizeof(uint2)), "alloc plan tables");
-  CK(cudaMalloc(&pl.g, gt.size() * sizeof(uint2)), "alloc plan tables");
-  CK(cudaMemcpy(pl.g, gt.data(), gt.size() * sizeof(uint2), cudaMemcpyHostToDevice),
-     "upload plan tables");
-  CK(cudaMemcpy(pl.tlo_m, tlo.data(), tlo.size() * sizeof(u32), cudaMemcpyHostToDevice),
-     "upload plan tables");
-  CK(cudaMemcpy(pl.thi, thi.data(), thi.size() * sizeof(uint2), cudaMemcpyHostToDevice),
-     "upload plan tables");
+  int rc;
+  if ((rc = upload((void**)&pl.tlo_m, tlo.data(), tlo.size() * sizeof(u32)))) return rc;
+  if ((rc = upload((void**)&pl.thi, thi.data(), thi.size() * sizeof(uint2)))) return rc;
+  if ((rc = upload((void**)&pl.g, gt.data(), gt.size() * sizeof(uint2)))) return rc;
+  if ((rc = upload((void**)&pl.trad, trad.data(), trad.size() * sizeof(uint2)))) return rc;
   // full four-step twiddle tables for small L (<= 2^kTw4MaxLg): 48 L bytes, L2-resident
-  if (pl.lgR > 0 && lg <= kTw4MaxLg) {
-    const size_t L = (size_t)1 << lg;
-    const int C = 1 << pl.lgC, R = 1 << pl.lgR;
+  if (R > 1 && L <= ((u64)1 << kTw4MaxLg)) {
     std::vector<uint2> t4((size_t)kNumPrimes * 2 * L);
     for (int i = 0; i < kNumPrimes; ++i) {
       const u32 p = kPrimes[i];
       for (int dir = 0; dir < 2; ++dir) {
-        const u32 wL = root_pow2(i, lg, dir);
+        const u32 wL = root_of(i, L, dir);
         uint2* t = &t4[((size_t)i * 2 + dir) * L];
         for (int q = 0; q < R; ++q) {
-          int k1 = 0;  // bit reversal of q in lgR bits
-          for (int b = 0; b < pl.lgR; ++b) k1 |= ((q >> b) & 1) << (pl.lgR - 1 - b);
+          // column frequency of storage row q (conv_kernels.cuh: row_k1)
+          const int k1 = (q >> geo.lgR) + geo.m * bitrev(q & ((1 << geo.lgR) - 1), geo.lgR);
           const u64 step = powmod(wL, (u64)k1, p);
           u64 x = 1;
           for (int c = 0; c < C; ++c) {
@@ -261,11 +327,9 @@ int get_plan(DevState* ds, int lg, const Plan** out) {
         }
       }
     }
-    CK(cudaMalloc(&pl.tw4, t4.size() * sizeof(uint2)), "alloc twiddle tables");
-    CK(cudaMemcpy(pl.tw4, t4.data(), t4.size() * sizeof(uint2), cudaMemcpyHostToDevice),
-       "upload twiddle tables");
+    if ((rc = upload((void**)&pl.tw4, t4.data(), t4.size() * sizeof(uint2)))) return rc;
   }
-  auto res = ds->plans.emplace(lg, pl);
+  auto res = ds->plans.emplace(key, pl);
   *out = &res.first->second;
   return PAB_OK;
 }
@@ -275,7 +339,10 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   t.stw = ds->stw;
   t.tlo_m = pl->tlo_m;
   t.thi = pl->thi;
+  t.thi_stride = pl->thi_stride;
   t.g = pl->g;
+  t.trad = pl->trad;
+  t.tstride = pl->tstride;
   t.tw4 = pl->tw4;
   for (int i = 0; i < kNumPrimes; ++i) {
     t.scale[i] = pl->scale[i];
@@ -284,22 +351,14 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   return t;
 }
 
-// P = p0 p1 p2 as a double-free bound check: k * (2^32-1)^2 < P.
+// exact three-prime convolution: k * (2^32-1)^2 < P = p0 p1 p2
 bool crt_bound_ok(u64 k) {
-  // compare with 128-bit arithmetic: P / (2^32-1)^2 ~ 2^25.35
   unsigned __int128 P = (unsigned __int128)kPrimes[0] * kPrimes[1] * kPrimes[2];
   unsigned __int128 w = (unsigned __int128)0xFFFFFFFFu * 0xFFFFFFFFu;
   return (unsigned __int128)k * w < P;
 }
 
-int lg_for(u64 len) {  // smallest lg with 2^lg >= len, at least 6
-  int lg = 6;
-  while (((u64)1 << lg) < len) ++lg;
-  return lg;
-}
-
-constexpr u64 kMaxChunk = 16384;
-  // blocks per launch (grid.y/z <= 65535)
+constexpr u64 kMaxChunk = 16384;  // blocks per launch (grid.y/z <= 65535)
 
 u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 u64 round_up(u64 a, u64 b) { return ceil_div(a, b) * b; }
@@ -313,10 +372,10 @@ struct Layout {
   size_t off_words, off_buf, off_out, off_state, off_ctr, total;
 };
 
-Layout layout_for(u64 kmax, int lg, u64 nT, u64 mw, u64 batch) {
+Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch) {
   Layout ly;
   ly.in_stride = round_up(kmax > 0 ? kmax : 1, 64);
-  ly.L = (u64)1 << lg;
+  ly.L = L;
   ly.tiles = ceil_div(nT, kCarryTile);
   ly.mw = mw;
   size_t off = 0;
@@ -336,7 +395,7 @@ Layout layout_for(u64 kmax, int lg, u64 nT, u64 mw, u64 batch) {
 
 struct HashGeo {
   u64 K;    // words per operand
-  int lg;
+  Geo geo;
   u64 mw;
 };
 
@@ -345,21 +404,22 @@ int hash_geo(u64 n, u64 r, HashGeo* g) {
   if (r < 1 || r > n) return fail(PAB_EINVAL, "output length r must satisfy 1 <= r <= n");
   if (n > pab_max_bits()) return fail(PAB_ERANGE, "block length exceeds pab_max_bits()");
   g->K = ceil_div(n, 32);
-  g->lg = lg_for(2 * g->K - 1);
+  if (!choose_geo(2 * g->K - 1, &g->geo))
+    return fail(PAB_ERANGE, "no transform geometry for this block length");
   g->mw = ceil_div(r, 32);
   return PAB_OK;
 }
 
-ConvJob make_job(const Layout& ly, void* ws, int lg, int batch) {
+ConvJob make_job(const Layout& ly, void* ws, const Geo& geo, int batch) {
   ConvJob j;
   std::memset(&j, 0, sizeof(j));
   char* base = (char*)ws;
   j.batch = batch;
-  j.lg = lg;
-  int lgR, lgC;
-  split_lg(lg, &lgR, &lgC);
-  j.lgR = lgR;
-  j.lgC = lgC;
+  j.m = geo.m;
+  j.lg = geo.lg;
+  j.lgR = geo.lgR;
+  j.lgC = geo.lgC;
+  j.L = (long long)geo.L;
   j.buf = (u32*)(base + ly.off_buf);
   j.out_words = (u32*)(base + ly.off_out);
   j.mw = (long long)ly.mw;
@@ -377,21 +437,21 @@ bool aligned4(const void* p) { return ((uintptr_t)p & 3) == 0; }
 // ================================================================== C ABI
 extern "C" {
 
-int pab_version(void) { return 100; }
+int pab_version(void) { return 101; }
 
 const char* pab_last_error(void) { return g_err.c_str(); }
 
-uint64_t pab_max_bits(void) { return (uint64_t)32 << (kMaxLg - 1); }  // 2K-1 <= 2^23
+// 2K - 1 <= 5 * 2^22 (largest radix-5 length), K < 2^25 (CRT bound)
+uint64_t pab_max_bits(void) { return (uint64_t)32 * ((((uint64_t)5 << kMaxLg) + 1) / 2); }
 
-int pab_plan_info(uint64_t n_bits, int* lg, int* lg_rows, int* lg_cols) {
+int pab_plan_info(uint64_t n_bits, int* radix, int* lg, int* lg_rows, int* lg_cols) {
   HashGeo g;
   int rc = hash_geo(n_bits, 1, &g);
   if (rc) return rc;
-  int a, b;
-  split_lg(g.lg, &a, &b);
-  if (lg) *lg = g.lg;
-  if (lg_rows) *lg_rows = a;
-  if (lg_cols) *lg_cols = b;
+  if (radix) *radix = g.geo.m;
+  if (lg) *lg = g.geo.lg;
+  if (lg_rows) *lg_rows = g.geo.lgR;
+  if (lg_cols) *lg_cols = g.geo.lgC;
   return PAB_OK;
 }
 
@@ -399,7 +459,7 @@ size_t pab_hash_workspace_bytes(uint64_t n_bits, uint32_t batch) {
   HashGeo g;
   if (hash_geo(n_bits, 1, &g)) return 0;
   // output words are bounded by K; size for the largest r
-  return layout_for(g.K, g.lg, g.K, g.K, batch ? batch : 1).total;
+  return layout_for(g.K, g.geo.L, g.K, g.K, batch ? batch : 1).total;
 }
 
 int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t in_stride,
@@ -419,12 +479,12 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   DevState* ds;
   if ((rc = current_device(&ds))) return rc;
   const Plan* pl;
-  if ((rc = get_plan(ds, g.lg, &pl))) return rc;
+  if ((rc = get_plan(ds, g.geo, &pl))) return rc;
   const PlanTables tab = tables_of(ds, pl);
   cudaStream_t st = (cudaStream_t)stream;
   // blocks per chunk that fit the workspace
   u64 chunk = batch < kMaxChunk ? batch : kMaxChunk;  // grid y/z limits
-  while (chunk > 0 && layout_for(g.K, g.lg, g.K, g.mw, chunk).total > workspace_bytes) chunk /= 2;
+  while (chunk > 0 && layout_for(g.K, g.geo.L, g.K, g.mw, chunk).total > workspace_bytes) chunk /= 2;
   if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
   const int msf = byte_order == PAB_ORDER_MSF;
   // LSF blocks whose words can be read in place (the common case): no pack kernel
@@ -434,8 +494,8 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   const u32 mask = (n_bits & 31) ? ((1u << (n_bits & 31)) - 1u) : 0xFFFFFFFFu;
   for (u64 b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = (int)((batch - b0) < chunk ? (batch - b0) : chunk);
-    const Layout ly = layout_for(g.K, g.lg, g.K, g.mw, nb);
-    ConvJob job = make_job(ly, workspace, g.lg, nb);
+    const Layout ly = layout_for(g.K, g.geo.L, g.K, g.mw, nb);
+    ConvJob job = make_job(ly, workspace, g.geo, nb);
     job.kA = job.kX = job.kD = (long long)g.K;
     job.maskA = job.maskX = job.maskD = mask;
     job.nT = (long long)g.K;
@@ -565,8 +625,9 @@ size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes) {
   const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4);
   if (ka == 0 || kb == 0) return 256;
   const u64 nT = ka + kb;
-  const int lg = lg_for(ka + kb - 1);
-  return layout_for(ka > kb ? ka : kb, lg, nT, nT, 1).total;
+  Geo geo;
+  if (!choose_geo(ka + kb - 1, &geo)) return 0;
+  return layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1).total;
 }
 
 int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes, uint8_t* out,
@@ -579,17 +640,17 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
     return PAB_OK;
   }
   const u64 nT = ka + kb;
-  const int lg = lg_for(ka + kb - 1);
-  if (lg > kMaxLg || !crt_bound_ok(ka < kb ? ka : kb))
+  Geo geo;
+  if (!choose_geo(ka + kb - 1, &geo) || !crt_bound_ok(ka < kb ? ka : kb))
     return fail(PAB_ERANGE, "operands exceed the exact three-prime convolution range");
-  const Layout ly = layout_for(ka > kb ? ka : kb, lg, nT, nT, 1);
+  const Layout ly = layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1);
   if (workspace_bytes < ly.total) return fail(PAB_EINVAL, "workspace too small");
   int rc;
   DevState* ds;
   if ((rc = current_device(&ds))) return rc;
   const Plan* pl;
-  if ((rc = get_plan(ds, lg, &pl))) return rc;
-  ConvJob job = make_job(ly, workspace, lg, 1);
+  if ((rc = get_plan(ds, geo, &pl))) return rc;
+  ConvJob job = make_job(ly, workspace, geo, 1);
   job.kA = (long long)ka;
   job.kX = (long long)kb;
   job.kD = 0;

@@ -266,7 +266,7 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
                                           u32 cin_seq) {
   constexpr int NR = kCarryRows;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long L = 1ll << job.lg;
+  const long long L = job.L;
   const u32* res0 = job.buf + (((long long)b * 2 + 0) * 3 + 0) * L;
   const u32* res1 = res0 + L;
   const u32* res2 = res1 + L;
@@ -597,12 +597,21 @@ static ConvKernels conv_for(int lg) {
     case 10: return conv_kernels_10();
     case 11: return conv_kernels_11();
     case 12: return conv_kernels_12();
-    default: return ConvKernels{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    default: {
+      ConvKernels k{};
+      return k;
+    }
   }
 }
 static ConvKernel row_kernel(int lg, bool small) {
   const ConvKernels k = conv_for(lg);
   return small ? k.row_small : k.row;
+}
+static ConvKernel colm_kernel(int m, int lgR, bool inv) {
+  if (lgR < 3 || lgR > 10 || (m != 3 && m != 5)) return nullptr;
+  const ConvKernels k = conv_for(lgR);
+  const int i = m == 3 ? 0 : 1;
+  return inv ? k.colm_inv[i] : k.colm_fwd[i];
 }
 static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
   if (lgR < 6) return nullptr;
@@ -620,20 +629,29 @@ static int col_lct(int lgR, int lgC) {
   return lct;
 }
 
+static int col_lct_rows(long long R, int lgC) {  // ~16K words (R rows x CT columns) per CTA
+  int lct = 5;
+  while (lct > 3 && (R << lct) > 16384) --lct;
+  if (lct > lgC) lct = lgC;
+  return lct;
+}
+
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
-  if (job.lgR == 0) {
+  if (job.m == 1 && job.lgR == 0) {
     const size_t sm = (size_t)sm_len(job.lgC) * 2 * 4;
     prof::Scope ps_("k_row_single", st);
     row_kernel(job.lgC, true)<<<dim3(1, kNumPrimes, job.batch), threads, sm, st>>>(job, tab, 0);
     return;
   }
-  const int lct = col_lct(job.lgR, job.lgC);
-  const size_t smc = (size_t)sm_len(job.lgR) * (1u << lct) * 4;
+  const long long R = (long long)job.m << job.lgR;
+  const int lct = job.m == 1 ? col_lct(job.lgR, job.lgC) : col_lct_rows(R, job.lgC);
+  const size_t smc = (size_t)job.m * sm_len(job.lgR) * (1u << lct) * 4;
+  ConvKernel cf = job.m == 1 ? col_kernel(job.lgR, job.lgC, false) : colm_kernel(job.m, job.lgR, false);
+  ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true) : colm_kernel(job.m, job.lgR, true);
   {
     prof::Scope ps_("k_col_fwd", st);
-    col_kernel(job.lgR, job.lgC, false)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads,
-                                 smc, st>>>(job, tab, lct);
+    cf<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(job, tab, lct);
   }
   int lnr = 13 - job.lgC;  // 8K words of rows (A+X: 16K words) per CTA
   if (lnr < 0) lnr = 0;
@@ -641,14 +659,19 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    row_kernel(job.lgC, false)<<<dim3(1u << (job.lgR - lnr), kNumPrimes, job.batch), threads, smr,
+    row_kernel(job.lgC, false)<<<dim3((unsigned)(R >> lnr), kNumPrimes, job.batch), threads, smr,
                                  st>>>(job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    col_kernel(job.lgR, job.lgC, true)<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc,
-                                st>>>(job, tab, lct);
+    ci<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc, st>>>(job, tab, lct);
   }
+}
+
+bool conv_supported(int m, int lgR, int lgC) {
+  if (m == 1 && lgR == 0) return row_kernel(lgC, true) != nullptr;
+  const ConvKernel cf = m == 1 ? col_kernel(lgR, lgC, false) : colm_kernel(m, lgR, false);
+  return cf != nullptr && row_kernel(lgC, false) != nullptr;
 }
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
@@ -668,6 +691,10 @@ void set_kernel_attrs() {
       if (k) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       for (int dc = 0; dc < 2; ++dc) {
         ConvKernel c = col_kernel(lg, lg + dc, s != 0);
+        if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      }
+      for (int m = 3; m <= 5; m += 2) {
+        ConvKernel c = colm_kernel(m, lg, s != 0);
         if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
     }

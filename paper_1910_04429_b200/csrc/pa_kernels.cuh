@@ -10,9 +10,12 @@ namespace pab {
 // All arrays are [prime][dir][4096] with dir 0 = forward (w), 1 = inverse (w^-1).
 struct PlanTables {
   const uint2* stw;    // stage twiddles tw[h+e] = w_{2h}^e (Shoup pairs), h <= 2048
-  const u32* tlo_m;    // Montgomery form of w_L^e, e < 4096
-  const uint2* thi;    // Shoup pairs of w_L^(4096 j)
-  const uint2* g;      // Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row-pass twiddle step)
+  const u32* tlo_m;    // [3][2][4096] Montgomery form of w_L^e, e < 4096
+  const uint2* thi;    // [3][2][thi_stride] Shoup pairs of w_L^(4096 j)
+  const uint2* g;      // [3][2][R] Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row twiddle step)
+  const uint2* trad;   // [3][2][R] Shoup pairs of w_R^e, e < R (radix-m column stage), or null
+  int tstride;         // R: stride of g and trad
+  int thi_stride;      // stride of thi (>= L / 4096)
   const uint2* tw4;    // [3][2][L] full four-step twiddles w_L^(+-c*brev(q)) at [q*C + c],
                        // Shoup pairs; only for small L (L2-resident), else null
   u32 scale[3];        // L^-1 * 2^32 mod p: undoes the length and the Montgomery factor
@@ -31,7 +34,9 @@ struct CrtConst {
 //   T = (A * X + D) mod 2^n_mod_bits (as 32-bit words), out = T >> shift.
 struct ConvJob {
   int batch;
-  int lg, lgR, lgC;            // L = 2^lg = R * C (R = 1: single-CTA path)
+  int m;                       // radix of the column length: L = m * 2^lg
+  int lg, lgR, lgC;            // R = m * 2^lgR rows (columns of length R), C = 2^lgC
+  long long L;                 // transform length (R = 1: single-CTA path)
   // operands as little-endian 32-bit words; block b at src + b * src_stride
   const u32* srcA;
   const u32* srcX;
@@ -77,5 +82,7 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st);
 // CRT + carry + mask + shift -> output.
 void launch_carry(const ConvJob& job, cudaStream_t st);
+// a kernel set exists for this geometry (L = m * 2^(lgR + lgC))
+bool conv_supported(int m, int lgR, int lgC);
 
 }  // namespace pab

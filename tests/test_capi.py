@@ -40,15 +40,21 @@ def test_sm100a_code_present():
 
 def test_host_only_queries():
     lib = _native.load()
-    assert lib.pab_version() == 100
-    assert _native.max_bits() == 1 << 27
-    assert _native.plan_info(10**6) == (16, 8, 8)
-    assert _native.plan_info(10**7) == (20, 10, 10)
-    assert _native.plan_info(10**8) == (23, 11, 12)
-    assert _native.plan_info(4) == (6, 0, 6)
+    assert lib.pab_version() == 101
+    assert _native.max_bits() == 32 * ((5 * 2**22 + 1) // 2)
+    # L = m * 2^lg: pow2 at 1e6, radix-5 at 1e7 (655360), radix-3 at 1e8 (6291456)
+    assert _native.plan_info(10**6) == (1, 16, 8, 8)
+    assert _native.plan_info(10**7) == (5, 17, 7, 10)
+    assert _native.plan_info(10**8) == (3, 21, 9, 12)
+    assert _native.plan_info(4) == (1, 6, 0, 6)
+    for n in (1, 33, 2047, 2049, 65537, 131_072 * 32, 3 * 10**6, 5 * 10**7, 1 << 27,
+              _native.max_bits()):
+        m, lg, lr, lc = _native.plan_info(n)
+        K = (n + 31) // 32
+        assert (m << lg) >= 2 * K - 1 and m in (1, 3, 5)
     assert lib.pab_hash_workspace_bytes(10**6, 1) > 6 * 4 * (1 << 16)
     assert lib.pab_hash_workspace_bytes(0, 1) == 0
-    rc = lib.pab_plan_info(0, None, None, None)
+    rc = lib.pab_plan_info(0, None, None, None, None)
     assert rc == _native.PAB_EINVAL
     assert b"block length" in lib.pab_last_error()
-    assert lib.pab_plan_info((1 << 27) + 1, None, None, None) == _native.PAB_ERANGE
+    assert lib.pab_plan_info(_native.max_bits() + 1, None, None, None, None) == _native.PAB_ERANGE
