@@ -147,6 +147,40 @@ def test_max_size_and_range_errors(n):
             _native.hash_host(x + b"\0", bytes(c) + b"\0", d + b"\0", n + 1, 5)
 
 
+def _plan_sweep_sizes():
+    """One block size per distinct (radix, lg_rows, lg_cols) plan up to 2^27 bits."""
+    seen, sizes = set(), []
+    n = 2000
+    while n < (1 << 27):
+        key = _native.plan_info(n)
+        if key not in seen:
+            seen.add(key)
+            sizes.append(n)
+        n = int(n * 1.09) + 7
+    return sizes
+
+
+def test_every_transform_plan_matches_oracle():
+    sizes = _plan_sweep_sizes()
+    radices = {_native.plan_info(n)[0] for n in sizes}
+    assert radices == {1, 3, 5}, radices
+    rng = np.random.default_rng(77)
+    for n in sizes:
+        r = int(rng.integers(1, n + 1))
+        nb = (n + 7) // 8
+        nblk = 2 if n < (1 << 24) else 1
+        arr = rng.integers(0, 256, size=(3, nblk, nb), dtype=np.uint8)
+        if n % 8:
+            arr[:, :, -1] &= (1 << (n % 8)) - 1
+        arr[1, :, 0] |= 1
+        dx, dc, dd = (torch.from_numpy(a).cuda() for a in arr)
+        out = HashEngine(n, r, max_batch=2).hash_device(dx, dc, dd).cpu().numpy()
+        for i in range(nblk):
+            want = oracle.compress(arr[0, i].tobytes(), arr[1, i].tobytes(), arr[2, i].tobytes(),
+                                   n, r)
+            assert out[i].tobytes() == want, (n, r, _native.plan_info(n))
+
+
 def test_msf_large_block():
     n, r = 3_000_001, 1_234_567
     rng = random.Random(12)
