@@ -275,17 +275,40 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   const long long wb = tbase + (long long)warp * NR * 32;  // first word of this warp
   const long long nres = job.nRes;
 
-  // issue every load of the tile first (memory-level parallelism), then CRT
+  // issue every load of the tile first (memory-level parallelism), then CRT.
+  // Warps entirely inside the valid ranges skip all per-word bounds checks.
   u32 V0[NR], V1[NR], V2[NR], DV[NR];
   const long long kd = dw ? job.kD : 0;
+  const bool in_res = wb + NR * 32 <= nres;
+  const bool in_d = wb + NR * 32 < kd;
+  if (in_res) {
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const long long k = wb + i * 32 + lane;
-    const bool ok = k < nres;
-    V0[i] = ok ? __ldg(res0 + k) : 0u;
-    V1[i] = ok ? __ldg(res1 + k) : 0u;
-    V2[i] = ok ? __ldg(res2 + k) : 0u;
-    DV[i] = k < kd ? __ldg(dw + k) : 0u;
+    for (int i = 0; i < NR; ++i) {
+      const long long k = wb + i * 32 + lane;
+      V0[i] = __ldg(res0 + k);
+      V1[i] = __ldg(res1 + k);
+      V2[i] = __ldg(res2 + k);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const long long k = wb + i * 32 + lane;
+      const bool ok = k < nres;
+      V0[i] = ok ? __ldg(res0 + k) : 0u;
+      V1[i] = ok ? __ldg(res1 + k) : 0u;
+      V2[i] = ok ? __ldg(res2 + k) : 0u;
+    }
+  }
+  if (in_d) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) DV[i] = __ldg(dw + wb + i * 32 + lane);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const long long k = wb + i * 32 + lane;
+      DV[i] = k < kd ? __ldg(dw + k) : 0u;
+      if (k == kd - 1) DV[i] &= job.maskD;
+    }
   }
   // virtual row -1 (lanes 30, 31 hold coefficients wb-2, wb-1)
   u32 P1 = 0, P2 = 0;
@@ -299,12 +322,11 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
     if (!ok) P1 = P2 = 0u;
   }
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const long long k = wb + i * 32 + lane;
-    const bool ok = k < nres;
-    crt3(V0[i], V1[i], V2[i], V0[i], V1[i], V2[i]);
-    if (!ok) V0[i] = V1[i] = V2[i] = 0u;
-    if (k == kd - 1) DV[i] &= job.maskD;
+  for (int i = 0; i < NR; ++i) crt3(V0[i], V1[i], V2[i], V0[i], V1[i], V2[i]);
+  if (!in_res) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+      if (wb + i * 32 + lane >= nres) V0[i] = V1[i] = V2[i] = 0u;
   }
   // column sums S_k = V0[k] + V1[k-1] + V2[k-2] + d[k]
   u64 S[NR];
@@ -400,8 +422,13 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   for (int i = 0; i < NR; ++i) {
     unsigned ones;
     T[i] = carry_row(S[i], c, ones);
-    const long long w = wb + i * 32 + lane;
-    T[i] = w >= nT ? 0u : (w == nT - 1 ? (T[i] & tmask) : T[i]);
+  }
+  if (wb + NR * 32 >= nT) {  // the warp reaches the top word: clear bits >= n_mod_bits
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const long long w = wb + i * 32 + lane;
+      T[i] = w >= nT ? 0u : (w == nT - 1 ? (T[i] & tmask) : T[i]);
+    }
   }
   // word after this warp's last word: next warp's first word, or (last warp)
   // the next tile's first word = S_next + carry
@@ -426,21 +453,31 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   const int sh = (int)(job.shift & 31);
   uint8_t* outb = job.out_words ? nullptr : job.out_bytes + (long long)b * job.out_stride;
   u32* outw = job.out_words ? job.out_words + (long long)b * job.mw : nullptr;
+  const long long o0 = wb - ws;
+  const bool out_full = o0 >= 0 && o0 + NR * 32 <= job.mw &&
+                        (outw != nullptr || 4 * (o0 + NR * 32) <= job.rbytes);
+  if (sh == 0 && out_full) {  // word-aligned shift, whole warp inside the key: plain stores
+    u32* ow = outw ? outw : reinterpret_cast<u32*>(outb);
 #pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const u32 up = __shfl_down_sync(0xFFFFFFFFu, T[i], 1);
-    const u32 nx = i + 1 < NR ? T[i + 1] : nextw;
-    const u32 wrap = __shfl_sync(0xFFFFFFFFu, nx, 0);
-    const u32 hiw = lane < 31 ? up : (i + 1 < NR ? wrap : nextw);
-    const long long oj = wb + i * 32 + lane - ws;
-    if (oj >= 0 && oj < job.mw) {
-      const u32 y = sh ? ((T[i] >> sh) | (hiw << (32 - sh))) : T[i];
-      if (outw) {
-        outw[oj] = y;
-      } else if (4 * oj + 4 <= job.rbytes) {
-        reinterpret_cast<u32*>(outb)[oj] = y;
-      } else {
-        for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q) outb[4 * oj + q] = (uint8_t)(y >> (8 * q));
+    for (int i = 0; i < NR; ++i) ow[o0 + i * 32 + lane] = T[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const u32 up = __shfl_down_sync(0xFFFFFFFFu, T[i], 1);
+      const u32 nx = i + 1 < NR ? T[i + 1] : nextw;
+      const u32 wrap = __shfl_sync(0xFFFFFFFFu, nx, 0);
+      const u32 hiw = lane < 31 ? up : (i + 1 < NR ? wrap : nextw);
+      const long long oj = o0 + i * 32 + lane;
+      if (oj >= 0 && oj < job.mw) {
+        const u32 y = sh ? ((T[i] >> sh) | (hiw << (32 - sh))) : T[i];
+        if (outw) {
+          outw[oj] = y;
+        } else if (4 * oj + 4 <= job.rbytes) {
+          reinterpret_cast<u32*>(outb)[oj] = y;
+        } else {
+          for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q)
+            outb[4 * oj + q] = (uint8_t)(y >> (8 * q));
+        }
       }
     }
   }
