@@ -299,9 +299,20 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
     return res
 
 
-def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int) -> tuple[dict, dict]:
+def ncu_traffic(workload: str | None) -> dict:
+    """Per-launch DRAM bytes of each kernel from the committed ncu capture of this workload."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not workload or not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        return json.load(f).get("workloads", {}).get(workload, {})
+
+
+def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int,
+                 workload: str | None = None) -> tuple[dict, dict]:
     model = kernel_model(n, r, blocks)
     pk = peaks()
+    traffic = ncu_traffic(workload)
     total = sum(v[1] for v in prof.values()) or 1.0
     kernels = {}
     for name, (cnt, ms) in prof.items():
@@ -320,7 +331,7 @@ def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int) -> tuple[d
         ach = mdl["bytes"] / avg_s / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
                 "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 4),
-                "traffic": None, "peak_src": pk["hbm_src"],
+                "traffic": traffic.get(dom), "peak_src": pk["hbm_src"],
                 "algorithmic_bytes_per_launch": mdl["bytes"]}
         if pk["int_tops"]:
             ach_ops = mdl["ops"] / avg_s / 1e12
@@ -386,7 +397,8 @@ def main():
 
     res = run_ours(args, cfg, rank, local_rank, world)
     n, r, per_rank = res["n"], res["r"], res["per_rank"]
-    roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk)
+    roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk,
+                                 workload=cfg["name"] if res["eng"].chunk == 1024 else None)
     launches = sum(v[0] for v in res["prof"].values())
 
     extra = {}
