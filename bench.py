@@ -175,6 +175,26 @@ def run_reference(args, cfg) -> dict:
             "sample": sample}
 
 
+def cpu_gmp_sample(cfg, xs, cs, ds, blocks: int) -> dict | None:
+    """Context row: the paper's own CPU method (GMP mpz sequence, oracle/gmp_ref.py)."""
+    try:
+        from oracle import gmp_ref
+    except Exception:  # pragma: no cover
+        return None
+    if not gmp_ref.available():
+        return None
+    n, r = cfg["n"], cfg["ms"][0]
+    threads = cpu_threads()
+    rows = [(xs[i].tobytes(), cs[i].tobytes(), ds[i].tobytes()) for i in range(blocks)]
+    t0 = time.perf_counter()
+    gmp_ref.compress_batch([a for a, _, _ in rows], [b for _, b, _ in rows],
+                           [c for _, _, c in rows], n, r, threads)
+    dt = time.perf_counter() - t0
+    return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps", "cores": threads,
+            "kind": "gmp (paper's method, PAPER.md:205-267)",
+            "sample": f"{blocks} blocks of {cfg['name']}, {dt:.2f}s wall"}
+
+
 def cpu_baseline_sample(cfg) -> dict:
     """Bounded sample of the workload on the oracle port (rank 0, N=1 only)."""
     import oracle
@@ -187,10 +207,11 @@ def cpu_baseline_sample(cfg) -> dict:
     t0 = time.perf_counter()
     out = oracle.compress_batch(xs.tobytes(), cs.tobytes(), ds.tobytes(), n, r, blocks, threads)
     dt = time.perf_counter() - t0
+    gmp = cpu_gmp_sample(cfg, xs, cs, ds, blocks)
     return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps", "cores": threads,
             "kind": "port",
             "sample": f"{blocks} blocks of {cfg['name']} (n={n}, r={r}), {dt:.2f}s wall",
-            "_out": out, "_blocks": blocks}
+            "context_gmp": gmp, "_out": out, "_blocks": blocks}
 
 
 # ------------------------------------------------------------------ GPU arm

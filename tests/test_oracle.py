@@ -93,3 +93,20 @@ def test_oracle_config_C4(config_golden):
 
 def test_oracle_config_C5_one_block_three_ratios(config_golden):
     _check_blocks(config_golden, "C5", [5])
+
+
+def test_gmp_context_matches_reference(small_golden, config_golden):
+    # the paper's GMP call sequence (oracle/gmp_ref.py) against reference outputs
+    from oracle import gmp_ref
+
+    if not gmp_ref.available():
+        pytest.skip("libgmp not present")
+    for case in small_golden["hash"]:
+        if case["order"] != "lsf":
+            continue
+        y = gmp_ref.compress(bytes.fromhex(case["x"]), bytes.fromhex(case["c"]),
+                             bytes.fromhex(case["d"]), case["n"], case["r"])
+        assert y.hex() == case["y"], (case["tag"], case["n"])
+    rec = config_golden["C1"]["blocks"][0]
+    x, c, d = workloads.block_inputs(10**6, rec["seed"])
+    assert sha(gmp_ref.compress(x, c, d, 10**6, 500_000)) == rec["out"]["500000"]
