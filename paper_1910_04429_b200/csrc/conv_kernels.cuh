@@ -11,7 +11,8 @@ struct ConvKernels {
   ConvKernel row, row_small;
   ConvKernel col_fwd, col_inv;      // column passes with lgC == LG (lg even)
   ConvKernel col_fwd1, col_inv1;    // column passes with lgC == LG + 1 (lg odd)
-  ConvKernel colm_fwd[2], colm_inv[2];  // mixed radix M = 3, 5 with LGR2 == LG (lgC runtime)
+  // mixed radix M = 3, 5 (index 0, 1) with LGR2 == LG and lgC = LG + 2 + dc (dc = 0..2)
+  ConvKernel colm_fwd[2][3], colm_inv[2][3];
 };
 
 __device__ __forceinline__ int brev(int x, int bits) {
@@ -487,14 +488,14 @@ __device__ __forceinline__ void colm_pass(u32* smem, int lct, const uint2* __res
   }
 }
 
-template <int P, int M, int LGR2>
+template <int P, int M, int LGR2, int LGC>
 __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR2);
   constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
   const int CT = 1 << lct;
   const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
-  const int lgC = job.lgC;
+  constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
   const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
@@ -547,14 +548,14 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
   }
 }
 
-template <int P, int M, int LGR2>
+template <int P, int M, int LGR2, int LGC>
 __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR2);
   constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
   const int CT = 1 << lct;
   const int b = blockIdx.z;
-  const int lgC = job.lgC;
+  constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
   const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
@@ -606,25 +607,25 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
   }
 }
 
-template <int M, int LGR2>
+template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(256) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
-    case 0: colm_fwd_body<0, M, LGR2>(job, tab, lct); break;
-    case 1: colm_fwd_body<1, M, LGR2>(job, tab, lct); break;
-    default: colm_fwd_body<2, M, LGR2>(job, tab, lct); break;
+    case 0: colm_fwd_body<0, M, LGR2, LGC>(job, tab, lct); break;
+    case 1: colm_fwd_body<1, M, LGR2, LGC>(job, tab, lct); break;
+    default: colm_fwd_body<2, M, LGR2, LGC>(job, tab, lct); break;
   }
 }
-template <int M, int LGR2>
+template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(256) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
-    case 0: colm_inv_body<0, M, LGR2>(job, tab, lct); break;
-    case 1: colm_inv_body<1, M, LGR2>(job, tab, lct); break;
-    default: colm_inv_body<2, M, LGR2>(job, tab, lct); break;
+    case 0: colm_inv_body<0, M, LGR2, LGC>(job, tab, lct); break;
+    case 1: colm_inv_body<1, M, LGR2, LGC>(job, tab, lct); break;
+    default: colm_inv_body<2, M, LGR2, LGC>(job, tab, lct); break;
   }
 }
 
 template <int LGR, int LGC>
-__global__ void __launch_bounds__(256) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
+__global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
     case 0: col_fwd_body<0, LGR, LGC>(job, tab, lct); break;
     case 1: col_fwd_body<1, LGR, LGC>(job, tab, lct); break;
@@ -658,10 +659,21 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
     k.col_inv1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_inv<R_, C1_> : nullptr;     \
     constexpr int M2_ = LG >= 3 && LG <= 10 ? LG : 3;                                 \
     const bool mx_ = LG >= 3 && LG <= 10;                                             \
-    k.colm_fwd[0] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_> : nullptr;                   \
-    k.colm_fwd[1] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_> : nullptr;                   \
-    k.colm_inv[0] = mx_ ? (ConvKernel)k_colm_inv<3, M2_> : nullptr;                   \
-    k.colm_inv[1] = mx_ ? (ConvKernel)k_colm_inv<5, M2_> : nullptr;                   \
+    constexpr int CA_ = M2_ + 2 <= 12 ? M2_ + 2 : 12;                                  \
+    constexpr int CB_ = M2_ + 3 <= 12 ? M2_ + 3 : 12;                                  \
+    constexpr int CC_ = M2_ + 4 <= 12 ? M2_ + 4 : 12;                                  \
+    k.colm_fwd[0][0] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CA_> : nullptr;           \
+    k.colm_fwd[0][1] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CB_> : nullptr;           \
+    k.colm_fwd[0][2] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CC_> : nullptr;           \
+    k.colm_fwd[1][0] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CA_> : nullptr;           \
+    k.colm_fwd[1][1] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CB_> : nullptr;           \
+    k.colm_fwd[1][2] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CC_> : nullptr;           \
+    k.colm_inv[0][0] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CA_> : nullptr;           \
+    k.colm_inv[0][1] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CB_> : nullptr;           \
+    k.colm_inv[0][2] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CC_> : nullptr;           \
+    k.colm_inv[1][0] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CA_> : nullptr;           \
+    k.colm_inv[1][1] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CB_> : nullptr;           \
+    k.colm_inv[1][2] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CC_> : nullptr;           \
     return k;                                                                        \
   }                                                                                  \
   }

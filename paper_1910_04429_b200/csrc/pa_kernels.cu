@@ -644,11 +644,12 @@ static ConvKernel row_kernel(int lg, bool small) {
   const ConvKernels k = conv_for(lg);
   return small ? k.row_small : k.row;
 }
-static ConvKernel colm_kernel(int m, int lgR, bool inv) {
-  if (lgR < 3 || lgR > 10 || (m != 3 && m != 5)) return nullptr;
+static ConvKernel colm_kernel(int m, int lgR, int lgC, bool inv) {
+  const int dc = lgC - lgR - 2;
+  if (lgR < 3 || lgR > 10 || (m != 3 && m != 5) || dc < 0 || dc > 2 || lgC > 12) return nullptr;
   const ConvKernels k = conv_for(lgR);
   const int i = m == 3 ? 0 : 1;
-  return inv ? k.colm_inv[i] : k.colm_fwd[i];
+  return inv ? k.colm_inv[i][dc] : k.colm_fwd[i][dc];
 }
 static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
   if (lgR < 6) return nullptr;
@@ -684,8 +685,10 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const long long R = (long long)job.m << job.lgR;
   const int lct = job.m == 1 ? col_lct(job.lgR, job.lgC) : col_lct_rows(R, job.lgC);
   const size_t smc = (size_t)job.m * sm_len(job.lgR) * (1u << lct) * 4;
-  ConvKernel cf = job.m == 1 ? col_kernel(job.lgR, job.lgC, false) : colm_kernel(job.m, job.lgR, false);
-  ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true) : colm_kernel(job.m, job.lgR, true);
+  ConvKernel cf = job.m == 1 ? col_kernel(job.lgR, job.lgC, false)
+                             : colm_kernel(job.m, job.lgR, job.lgC, false);
+  ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true)
+                             : colm_kernel(job.m, job.lgR, job.lgC, true);
   {
     prof::Scope ps_("k_col_fwd", st);
     cf<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(job, tab, lct);
@@ -707,7 +710,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
 
 bool conv_supported(int m, int lgR, int lgC) {
   if (m == 1 && lgR == 0) return row_kernel(lgC, true) != nullptr;
-  const ConvKernel cf = m == 1 ? col_kernel(lgR, lgC, false) : colm_kernel(m, lgR, false);
+  const ConvKernel cf = m == 1 ? col_kernel(lgR, lgC, false) : colm_kernel(m, lgR, lgC, false);
   return cf != nullptr && row_kernel(lgC, false) != nullptr;
 }
 
@@ -730,10 +733,11 @@ void set_kernel_attrs() {
         ConvKernel c = col_kernel(lg, lg + dc, s != 0);
         if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
-      for (int m = 3; m <= 5; m += 2) {
-        ConvKernel c = colm_kernel(m, lg, s != 0);
-        if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      }
+      for (int m = 3; m <= 5; m += 2)
+        for (int dc = 2; dc <= 4; ++dc) {
+          ConvKernel c = colm_kernel(m, lg, lg + dc, s != 0);
+          if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }
     }
   }
 }
