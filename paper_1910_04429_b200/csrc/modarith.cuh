@@ -25,13 +25,6 @@ constexpr int kMaxLg = 22;        // 2-adicity common to all three primes
 constexpr int kTwN = 4096;        // largest in-CTA sub-transform
 constexpr int kTwLg = 12;
 
-struct PrimeInfo {
-  u32 p;
-  u32 two_p;
-  u32 p_mont;   // -p^{-1} mod 2^32
-  u32 one_sh;   // floor(2^32 / p): Shoup companion of w = 1
-};
-
 #ifdef __CUDACC__
 // Shoup multiplication a*w mod p with precomputed wp = floor(w*2^32/p).
 // Any a < 2^32; result in [0, 2p).
@@ -53,34 +46,6 @@ __device__ __forceinline__ u32 montmul(u32 a, u32 b, u32 p, u32 p_mont) {
   return hi + mh + (lo != 0u ? 1u : 0u);
 }
 
-// Gentleman-Sande (DIF) butterfly: x, y in [0, 2p) -> x+y, (x-y)*w, both [0, 2p).
-__device__ __forceinline__ void dif_bfly(u32& x, u32& y, uint2 w, u32 p, u32 two_p) {
-  u32 s = red(x + y, two_p);
-  u32 d = x - y + two_p;
-  y = shoup(d, w, p);
-  x = s;
-}
-// DIF butterfly with twiddle 1.
-__device__ __forceinline__ void dif_bfly1(u32& x, u32& y, u32 two_p) {
-  u32 s = red(x + y, two_p);
-  u32 d = x - y + two_p;
-  y = red(d, two_p);
-  x = s;
-}
-// Cooley-Tukey (DIT) butterfly: x in [0, 4p), y < 2^32 -> x+w*y, x-w*y in [0, 4p).
-__device__ __forceinline__ void dit_bfly(u32& x, u32& y, uint2 w, u32 p, u32 two_p) {
-  u32 a = red(x, two_p);
-  u32 t = shoup(y, w, p);
-  x = a + t;
-  y = a - t + two_p;
-}
-// DIT butterfly with twiddle 1 (y must be < 4p).
-__device__ __forceinline__ void dit_bfly1(u32& x, u32& y, u32 two_p) {
-  u32 a = red(x, two_p);
-  u32 t = red(y, two_p);
-  x = a + t;
-  y = a - t + two_p;
-}
 #endif
 
 }  // namespace pab

@@ -64,16 +64,6 @@ u64 powmod(u64 a, u64 e, u64 m) {
 u32 inv_mod(u32 a, u32 p) { return (u32)powmod(a, p - 2, p); }
 u32 shoup_of(u32 w, u32 p) { return (u32)(((u64)w << 32) / p); }
 
-PrimeInfo prime_info(u32 p) {
-  PrimeInfo pi;
-  pi.p = p;
-  pi.two_p = 2 * p;
-  u32 inv = 1;  // p^-1 mod 2^32 by Newton
-  for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
-  pi.p_mont = 0u - inv;
-  pi.one_sh = shoup_of(1, p);
-  return pi;
-}
 
 // w_N = g^((p-1)/N) (dir 1: its inverse): the same roots the device code
 // derives at compile time (ntt_core.cuh: croot_n)
@@ -187,8 +177,6 @@ int ensure_device(int dev, DevState** out) {
       if (((p - 1) >> kMaxLg) << kMaxLg != p - 1)
         return fail(PAB_ECUDA, "internal: prime 2-adicity below kMaxLg");
     }
-    PrimeInfo pis[kNumPrimes];
-    for (int i = 0; i < kNumPrimes; ++i) pis[i] = prime_info(kPrimes[i]);
     CrtConst crt;
     crt.p0 = kPrimes[0];
     crt.p1 = kPrimes[1];
@@ -200,7 +188,7 @@ int ensure_device(int dev, DevState** out) {
     crt.inv012 = inv_mod((u32)(((u64)crt.p0 * crt.p1) % crt.p2), crt.p2);
     crt.inv012_sh = shoup_of(crt.inv012, crt.p2);
     crt.p0p1 = (u64)crt.p0 * crt.p1;
-    upload_constants(pis, crt);
+    upload_constants(crt);
     CK(cudaGetLastError(), "upload constants");
     // stage twiddles tw[h + e] = w_{2h}^{+-e}
     std::vector<uint2> stw((size_t)kNumPrimes * 2 * kTwN);

@@ -97,13 +97,9 @@ int profile_collect(const char** names, int* counts, double* ms, int cap) {
   return nn;
 }
 
-__constant__ PrimeInfo c_primes[kNumPrimes];
 __constant__ CrtConst c_crt;
 
-void upload_constants(const PrimeInfo* primes, const CrtConst& crt) {
-  cudaMemcpyToSymbol(c_primes, primes, sizeof(PrimeInfo) * kNumPrimes);
-  cudaMemcpyToSymbol(c_crt, &crt, sizeof(CrtConst));
-}
+void upload_constants(const CrtConst& crt) { cudaMemcpyToSymbol(c_crt, &crt, sizeof(CrtConst)); }
 
 // ---------------------------------------------------------------------------
 // pack / unpack (MSF byte order or unaligned blocks only)

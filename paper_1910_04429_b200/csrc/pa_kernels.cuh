@@ -66,7 +66,7 @@ constexpr int kCarryTile = 32 * kCarryWarps * kCarryRows;  // words per tile
 
 constexpr int kTinyBits = 2048;  // single-warp schoolbook path (n <= kTinyBits)
 
-void upload_constants(const PrimeInfo* primes, const CrtConst& crt);
+void upload_constants(const CrtConst& crt);
 void launch_tiny(const uint8_t* x, const uint8_t* c, const uint8_t* d, long long stride, int n_bits,
                  int r_bits, int msf, int batch, uint8_t* out, long long out_stride,
                  cudaStream_t st);
