@@ -124,3 +124,51 @@ class HashEngine:
                         for _ in range(k)]
             self._io_key = key
         return self._io
+
+
+def hash_host_multi(x: torch.Tensor, c: torch.Tensor, d: torch.Tensor, n: int, r: int, *,
+                    devices: list[int] | None = None, order: int = _native.ORDER_LSF,
+                    max_batch: int = 256) -> torch.Tensor:
+    """Hash a pinned host batch on several GPUs of this process: one worker thread per
+    device, contiguous block shards, keys returned in block order.
+
+    Blocks are independent (SURVEY.md §8e), so there is no inter-GPU traffic;
+    each worker runs HashEngine.hash_host on its shard (copies overlapped with
+    compute on that device's streams).  The C ABI releases the GIL, so the
+    workers run concurrently.
+    """
+    import threading
+
+    devs = list(range(torch.cuda.device_count())) if devices is None else list(devices)
+    if not devs:
+        raise _native.NativeUnavailable("no CUDA device (there is no CPU fallback)")
+    b = x.shape[0]
+    out = torch.empty((b, (r + 7) // 8), dtype=torch.uint8, pin_memory=True)
+    spans = []
+    base, extra = divmod(b, len(devs))
+    lo = 0
+    for i, dev in enumerate(devs):
+        hi = lo + base + (1 if i < extra else 0)
+        spans.append((dev, lo, hi))
+        lo = hi
+    errors = []
+
+    def work(dev, lo, hi):
+        try:
+            if hi <= lo:
+                return
+            torch.cuda.set_device(dev)
+            eng = HashEngine(n, r, device=dev, order=order, max_batch=min(max_batch, hi - lo))
+            eng.hash_host(x[lo:hi], c[lo:hi], d[lo:hi], out[lo:hi], streams=3)
+            torch.cuda.synchronize(dev)
+        except BaseException as e:  # surfaced in the caller
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=s) for s in spans]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out

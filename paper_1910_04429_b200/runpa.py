@@ -95,20 +95,21 @@ class PaRunResult:
 Hasher = Callable[[np.ndarray, np.ndarray, np.ndarray, int, int, WordOrder], np.ndarray]
 
 
-def gpu_hasher(batch: int = 256) -> Hasher:
-    """Default hasher: the CUDA path (HashEngine.hash_host over pinned staging)."""
+def gpu_hasher(batch: int = 256, devices: list[int] | None = None) -> Hasher:
+    """Default hasher: the CUDA path over pinned staging.  `devices` = GPUs of this
+    process to shard each batch over (default: the current device only; under
+    torch.distributed every rank owns one GPU)."""
 
     def run(x, c, d, n, r, order):
         import torch
 
-        from .batch import HashEngine
+        from .batch import hash_host_multi
 
-        eng = HashEngine(n, r, max_batch=min(batch, max(1, x.shape[0])),
-                         order=_native.ORDER_MSF if order is WordOrder.MOST_SIGNIFICANT_FIRST
-                         else _native.ORDER_LSF)
+        devs = devices if devices is not None else [torch.cuda.current_device()]
         px, pc, pd = (torch.from_numpy(np.array(a, copy=True)).pin_memory() for a in (x, c, d))
-        out = eng.hash_host(px, pc, pd, streams=3)
-        torch.cuda.synchronize()
+        out = hash_host_multi(px, pc, pd, n, r, devices=devs, max_batch=batch,
+                              order=_native.ORDER_MSF if order is WordOrder.MOST_SIGNIFICANT_FIRST
+                              else _native.ORDER_LSF)
         return out.numpy()
 
     return run

@@ -44,3 +44,22 @@ def test_compress_matches_direct_formula_random():
         s = pab.gen_seed(n, rng.randrange(1 << 30))
         want = ((s.c.value * x.value + s.d.value) % (1 << n)) >> (n - r)
         assert pab.compress(x, s, r).value == want, (n, r)
+
+
+def test_hash_host_multi_matches_single_device():
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1910_04429_b200.batch import hash_host_multi
+
+    n, r, B = 200_000, 77_777, 9
+    rng = np.random.default_rng(4)
+    arr = rng.integers(0, 256, size=(3, B, (n + 7) // 8), dtype=np.uint8)
+    arr[1, :, 0] |= 1
+    px, pc, pd = (torch.from_numpy(a).pin_memory() for a in arr)
+    devs = list(range(torch.cuda.device_count())) * 2  # a device may appear twice (two workers)
+    out = hash_host_multi(px, pc, pd, n, r, devices=devs, max_batch=2).numpy()
+    for i in range(B):
+        want = oracle.compress(arr[0, i].tobytes(), arr[1, i].tobytes(), arr[2, i].tobytes(), n, r)
+        assert out[i].tobytes() == want, i
