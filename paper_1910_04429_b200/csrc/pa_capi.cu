@@ -31,7 +31,7 @@ using namespace pab;
 namespace {
 
 thread_local std::string g_err;
-constexpr int kTw4MaxLg = 18;  // full four-step twiddle tables up to L = 2^18 (12 MiB, L2-resident)
+constexpr int kTw4MaxLg = 20;  // full four-step twiddle tables up to L = 2^20 (48 L bytes <= 48 MiB)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -295,7 +295,7 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   if ((rc = upload((void**)&pl.thi, thi.data(), thi.size() * sizeof(uint2)))) return rc;
   if ((rc = upload((void**)&pl.g, gt.data(), gt.size() * sizeof(uint2)))) return rc;
   if ((rc = upload((void**)&pl.trad, trad.data(), trad.size() * sizeof(uint2)))) return rc;
-  // full four-step twiddle tables for small L (<= 2^kTw4MaxLg): 48 L bytes, L2-resident
+  // full four-step twiddle tables (L <= 2^kTw4MaxLg): 48 L bytes, read once per launch
   if (R > 1 && L <= ((u64)1 << kTw4MaxLg)) {
     std::vector<uint2> t4((size_t)kNumPrimes * 2 * L);
     for (int i = 0; i < kNumPrimes; ++i) {
