@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(256) k_colm_fwd(ConvJob job, PlanTables tab, i
   }
 }
 template <int M, int LGR2, int LGC>
-__global__ void __launch_bounds__(256) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
+__global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
   switch (blockIdx.y) {
     case 0: colm_inv_body<0, M, LGR2, LGC>(job, tab, lct); break;
     case 1: colm_inv_body<1, M, LGR2, LGC>(job, tab, lct); break;

@@ -685,6 +685,16 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
                              : colm_kernel(job.m, job.lgR, job.lgC, false);
   ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true)
                              : colm_kernel(job.m, job.lgR, job.lgC, true);
+  // mixed-radix inverse: one thread per task of its first pow2 pass (M * CT * 2^(lgR-5)
+  // tasks; 256 threads would leave e.g. 384 tasks at 75% utilisation).  The forward
+  // kernel keeps 256 threads: its register count would halve the resident CTAs.
+  int ct_threads = threads;
+  if (job.m > 1) {
+    const int lastrs = pass_plan(job.lgR).rs[pass_plan(job.lgR).n - 1];
+    ct_threads = (job.m << lct) << (job.lgR - lastrs);
+    while (ct_threads > 512) ct_threads >>= 1;
+    if (ct_threads < 128) ct_threads = 128;
+  }
   {
     prof::Scope ps_("k_col_fwd", st);
     cf<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(job, tab, lct);
@@ -700,7 +710,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    ci<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), threads, smc, st>>>(job, tab, lct);
+    ci<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), ct_threads, smc, st>>>(job, tab, lct);
   }
 }
 
