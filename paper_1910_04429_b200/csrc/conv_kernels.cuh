@@ -505,6 +505,46 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
   const uint2* trad = tab.trad + (P * 2 + 0) * tab.tstride;
   const int lim = (int)(kv < L ? kv : L), ilast = (int)kv - 1;
+  constexpr bool FUSE = PP.n >= 2 && M * (1 << PP.rs[0]) <= 32;  // register budget
+  if constexpr (FUSE) {
+    // radix-M stage fused with the first pow2 pass (when M * 2^RS0 <= 32 values fit in
+    // registers without losing occupancy): a task (column t, offset o) loads
+    // the M * 2^RS0 words of rows {o + k*2^SLO0 + s*R2}, runs the 2^RS0 radix-M DFTs
+    // (+ twiddles w_R^(j*s)), then the top RS0 DIF stages of all M sub-columns with
+    // shared table twiddles, and stores once to smem.
+    constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      u32 v[M][1 << RS0];
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        const int j = o + (k << SLO0);
+        u32 a[M];
+#pragma unroll
+        for (int s = 0; s < M; ++s) {
+          const int gi = ((j + s * R2) << lgC) + c0 + t;
+          u32 w = gi < lim ? __ldg(src + gi) : 0u;
+          w &= gi == ilast ? mask : 0xFFFFFFFFu;
+          a[s] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+        }
+        radix_m<P, M, false>(a);
+#pragma unroll
+        for (int s = 0; s < M; ++s)
+          v[s][k] = s ? shoup(a[s], __ldg(trad + j * s), PK<P>::p) : a[0];
+      }
+      dif_rt<P, RS0, SLO0, M>(v, twf + o);
+#pragma unroll
+      for (int s = 0; s < M; ++s)
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k)
+          smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t] = v[s][k];
+    }
+    __syncthreads();
+    if constexpr (PP.n == 3) {
+      colm_pass<P, M, LGR2, PP.rs[1], PP.slo[1], true>(smem, lct, twf);
+      __syncthreads();
+    }
+  } else {
   // radix-M stage straight from the operand words
   for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
     const int t = task & (CT - 1), j = task >> lct;
@@ -530,6 +570,7 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
   if constexpr (PP.n == 3) {
     colm_pass<P, M, LGR2, PP.rs[1], PP.slo[1], true>(smem, lct, twf);
     __syncthreads();
+  }
   }
   // last pow2 pass (stages RSL-1..0, compile-time twiddles) -> global rows s*R2 + pos
   constexpr int RSL = PP.rs[PP.n - 1];
@@ -585,12 +626,43 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
     colm_pass<P, M, LGR2, PP.rs[1], PP.slo[1], false>(smem, lct, twi);
     __syncthreads();
   }
+  const int nres = (int)(job.nRes < L ? job.nRes : L);
+  constexpr bool FUSE = PP.n >= 2 && M * (1 << PP.rs[0]) <= 32;  // register budget
+  if constexpr (FUSE) {
+    // top pow2 DIT stages of the M sub-columns fused with the inverse radix-M stage
+    constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+      const int t = task & (CT - 1), o = task >> lct;
+      u32 v[M][1 << RS0];
+#pragma unroll
+      for (int s = 0; s < M; ++s) {
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k)
+          v[s][k] = smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t];
+        dit_rt<P, RS0, SLO0>(v[s], twi + o);
+      }
+#pragma unroll
+      for (int k = 0; k < (1 << RS0); ++k) {
+        const int j = o + (k << SLO0);
+        u32 a[M];
+        a[0] = red(v[0][k], PK<P>::two_p);
+#pragma unroll
+        for (int s = 1; s < M; ++s) a[s] = shoup(v[s][k], __ldg(trad + j * s), PK<P>::p);
+        radix_m<P, M, true>(a);
+#pragma unroll
+        for (int s = 0; s < M; ++s) {
+          const int gi = ((j + s * R2) << lgC) + c0 + t;
+          if (gi < nres) res[gi] = red(shoup(a[s], sc, sc_sh, PK<P>::p), PK<P>::p);
+        }
+      }
+    }
+    return;
+  }
   if constexpr (PP.n >= 2) {
     colm_pass<P, M, LGR2, PP.rs[0], PP.slo[0], false>(smem, lct, twi);
     __syncthreads();
   }
   // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT, scale -> residues
-  const int nres = (int)(job.nRes < L ? job.nRes : L);
   for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
     const int t = task & (CT - 1), j = task >> lct;
     u32 a[M];
