@@ -364,6 +364,25 @@ def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int,
     return roof, kernels
 
 
+def step_roofline(n: int, r: int, blocks: int, ms_step: float) -> dict | None:
+    """North-star roofline of a whole step: the slower of (canonical int ops at the
+    measured int peak) and (algorithmic HBM bytes at the measured copy bandwidth),
+    summed over the step's kernels, vs the measured step time."""
+    pk = peaks()
+    if not pk["int_tops"]:
+        return None
+    model = kernel_model(n, r, blocks)
+    ops = sum(v["ops"] for k, v in model.items() if k not in ("k_pack", "k_unpack"))
+    byts = sum(v["bytes"] for k, v in model.items() if k not in ("k_pack", "k_unpack"))
+    t_int = ops / (pk["int_tops"] * 1e12) * 1e3
+    t_hbm = byts / (pk["hbm_gbs"] * 1e9) * 1e3
+    t_roof = max(t_int, t_hbm)
+    return {"t_int_ms": round(t_int, 4), "t_hbm_ms": round(t_hbm, 4), "t_roof_ms": round(t_roof, 4),
+            "measured_ms": round(ms_step, 4), "frac": round(t_roof / ms_step, 4),
+            "bound": "int" if t_int >= t_hbm else "hbm",
+            "roofline_mbps": round(blocks * n / t_roof / 1e3, 1)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -420,6 +439,7 @@ def main():
     n, r, per_rank = res["n"], res["r"], res["per_rank"]
     roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk,
                                  workload=cfg["name"] if res["eng"].chunk == 1024 else None)
+    step_roof = step_roofline(n, r, per_rank, res["ms_step"])
     launches = sum(v[0] for v in res["prof"].values())
 
     extra = {}
@@ -449,6 +469,7 @@ def main():
                        "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
                              % (3 * per_rank * ((n + 7) // 8) / 1e6)},
             "e2e": res["e2e"], "gpu_launches": launches, "roofline": roof,
+            "step_roofline": step_roof,
             "kernels": kernels, "clocks": res["clocks"], "cpu_baseline": cpu,
         }
         if extra:
@@ -479,7 +500,8 @@ def side_1e8(args, dist) -> dict:
     roof, kernels = roofline_obj(prof, steps, n, r, B)
     return {"workload": "C5 subset: %d blocks/rank, n=1e8, r=5e7" % B,
             "value": round(world * B * n / (ms_step * 1e-3) / 1e6, 1), "unit": "Mbps",
-            "ms_per_step": round(ms_step, 3), "roofline": roof, "kernels": kernels}
+            "ms_per_step": round(ms_step, 3), "roofline": roof,
+            "step_roofline": step_roofline(n, r, B, ms_step), "kernels": kernels}
 
 
 if __name__ == "__main__":
