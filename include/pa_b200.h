@@ -57,6 +57,21 @@ uint64_t pab_max_bits(void);
 int pab_plan_info(uint64_t n_bits, int* radix, int* lg, int* lg_rows, int* lg_cols);
 
 /*
+ * Convolution mode chosen for an n-bit hash: coefficient width (64: two words
+ * per coefficient over five NTT primes, used up to 121,295,104 bits; 32: one
+ * word over three primes, beyond) and the number of primes.  Any pointer may
+ * be NULL.
+ */
+int pab_plan_width(uint64_t n_bits, int* coef_bits, int* primes);
+
+/*
+ * Test hook: force the coefficient width (1 or 2 words) wherever it is valid,
+ * 0 restores the automatic choice.  Process-wide; results are identical in
+ * every mode, only the work differs.
+ */
+void pab_force_coef_words(int words);
+
+/*
  * Device workspace needed to hash `batch` n-bit blocks in one pass.
  * pab_hash_batch processes larger batches in chunks that fit the workspace
  * it is given (at least one block must fit).

@@ -32,6 +32,8 @@ SIGNATURES = {
     "pab_last_error": (ctypes.c_char_p, []),
     "pab_max_bits": (ctypes.c_uint64, []),
     "pab_plan_info": (ctypes.c_int, [ctypes.c_uint64] + [ctypes.POINTER(ctypes.c_int)] * 4),
+    "pab_plan_width": (ctypes.c_int, [ctypes.c_uint64] + [ctypes.POINTER(ctypes.c_int)] * 2),
+    "pab_force_coef_words": (None, [ctypes.c_int]),
     "pab_hash_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint32]),
     "pab_hash_batch": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, _u8p,
@@ -134,6 +136,19 @@ def profile_collect() -> dict[str, tuple[int, float]]:
     ms = (ctypes.c_double * cap)()
     k = load().pab_profile_collect(names, counts, ms, cap)
     return {names[i].decode(): (counts[i], ms[i]) for i in range(k)}
+
+
+def plan_width(n: int) -> tuple[int, int]:
+    """(coefficient bits, NTT primes) of the convolution used for an n-bit hash."""
+    lib = load()
+    cb, np_ = ctypes.c_int(), ctypes.c_int()
+    check(lib.pab_plan_width(n, ctypes.byref(cb), ctypes.byref(np_)))
+    return cb.value, np_.value
+
+
+def force_coef_words(words: int) -> None:
+    """Test hook: force 1- or 2-word coefficients where valid (0 = automatic)."""
+    load().pab_force_coef_words(int(words))
 
 
 def max_bits() -> int:

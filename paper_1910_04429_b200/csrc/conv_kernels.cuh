@@ -19,13 +19,82 @@ __device__ __forceinline__ int brev(int x, int bits) {
   return bits == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - bits));
 }
 
-// operand word fetch: zero beyond the valid words, mask the last one
-__device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long gi, long long kv,
-                                          u32 mask) {
-  if (gi >= kv) return 0u;
-  const u32 w = __ldg(src + gi);
-  return gi == kv - 1 ? (w & mask) : w;
+// Operand in coefficient units: cw = 2 reads 64-bit coefficients (words 2i, 2i+1;
+// 8-byte aligned), cw = 1 single words.  Coefficients >= kc are zero; the last
+// one is masked with (mlo, mhi) (bits >= n of the operand's last word).
+struct OpView {
+  const u32* src;
+  int kc;
+  u32 mlo, mhi;
+  int cw;
+};
+__device__ __forceinline__ OpView op_view(const ConvJob& job, int op, int b) {
+  OpView v;
+  v.src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
+  const long long kv = op ? job.kX : job.kA;
+  const u32 mask = op ? job.maskX : job.maskA;
+  v.cw = job.cw;
+  if (job.cw == 2) {
+    v.kc = (int)((kv + 1) >> 1);
+    v.mlo = (kv & 1) ? mask : 0xFFFFFFFFu;
+    v.mhi = (kv & 1) ? 0u : mask;
+  } else {
+    v.kc = (int)kv;
+    v.mlo = mask;
+    v.mhi = 0u;
+  }
+  return v;
 }
+// coefficient (lo, hi) -> residue in [0, 2p)
+template <int P>
+__device__ __forceinline__ u32 coef_red(u32 lo, u32 hi, int cw) {
+  const u32 a = shoup(lo, 1u, PK<P>::one_sh, PK<P>::p);
+  if (cw == 1) return a;
+  return red(a + shoup(hi, PK<P>::r32, PK<P>::r32_sh, PK<P>::p), PK<P>::two_p);
+}
+// coefficient gi known to be valid and unmasked (gi < kc - 1)
+template <int P>
+__device__ __forceinline__ u32 coef_fast(const OpView& o, int gi) {
+  if (o.cw == 2) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+    return coef_red<P>(w.x, w.y, 2);
+  }
+  return coef_red<P>(__ldg(o.src + gi), 0u, 1);
+}
+// any coefficient index: zero at or beyond kc, last one masked
+template <int P>
+__device__ __forceinline__ u32 coef_at(const OpView& o, int gi) {
+  u32 lo = 0u, hi = 0u;
+  if (gi < o.kc) {
+    if (o.cw == 2) {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+      lo = w.x;
+      hi = w.y;
+    } else {
+      lo = __ldg(o.src + gi);
+    }
+    if (gi == o.kc - 1) {
+      lo &= o.mlo;
+      hi &= o.mhi;
+    }
+  }
+  return coef_red<P>(lo, hi, o.cw);
+}
+
+// conv kernels run one prime per grid index IDX (job.np of them).  Kernels
+// without cross-prime data reuse (row, inverse column) put the prime in the
+// slowest grid dimension so CTAs resident together run the same prime's
+// code: one body is ~20-40 KB of straight-line SASS, and mixing primes on an
+// SM starves instruction fetch (ncu: stall_no_instructions dominant).
+#define PAB_PRIME_SWITCH(X, IDX) \
+  switch (IDX) {                 \
+    case 0: X(0); break;         \
+    case 1: X(1); break;         \
+    case 2: X(2); break;         \
+    case 3: X(3); break;         \
+    default: X(4); break;        \
+  }
+static_assert(kNumPrimes == 5, "PAB_PRIME_SWITCH covers five primes");
 
 // four-step twiddle seed w_L^e * 2^32 (Montgomery form, lazy [0, 2p)), e < L
 template <int P>
@@ -53,7 +122,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
   constexpr int T = sm_len(LGC);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int NR = 1 << lnr;
-  const int b = blockIdx.z;
+  const int b = blockIdx.y;  // grid (R / NR, batch, prime)
   const int q0 = blockIdx.x << lnr;
   const int lgR = job.lgR;
   const long long L = job.L;
@@ -61,10 +130,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
   u32* sX = smem + NR * T;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
   const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
-  u32* gA = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;  // also the residue slot
-  u32* gX = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
-  const u32* wA = job.srcA + (long long)b * job.src_stride;
-  const u32* wX = job.srcX + (long long)b * job.src_stride;
+  u32* gA = job.buf + (((long long)b * 2 + 0) * job.np + P) * L;  // also the residue slot
+  u32* gX = job.buf + (((long long)b * 2 + 1) * job.np + P) * L;
+  const OpView vA = op_view(job, 0, b), vX = op_view(job, 1, b);
 
   // ---- pass 0: global -> (twiddle) -> DIF top stages -> smem (A and X share twiddles)
   if constexpr (PP.n > 1) {
@@ -75,9 +143,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
       if constexpr (SMALL) {
 #pragma unroll
         for (int k = 0; k < (1 << RS0); ++k) {
-          const long long gi = o + (k << SLO0);
-          v[0][k] = shoup(fetch_word(wA, gi, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
-          v[1][k] = shoup(fetch_word(wX, gi, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+          const int gi = o + (k << SLO0);
+          v[0][k] = coef_at<P>(vA, gi);
+          v[1][k] = coef_at<P>(vX, gi);
         }
       } else {
         const u32* ra = gA + ((long long)q << LGC) + o;
@@ -153,8 +221,8 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
         if constexpr (SMALL) {
 #pragma unroll
           for (int k = 0; k < (1 << RSL); ++k) {
-            a[0][k] = shoup(fetch_word(wA, k, job.kA, job.maskA), 1u, PK<P>::one_sh, PK<P>::p);
-            x[0][k] = shoup(fetch_word(wX, k, job.kX, job.maskX), 1u, PK<P>::one_sh, PK<P>::p);
+            a[0][k] = coef_at<P>(vA, k);
+            x[0][k] = coef_at<P>(vX, k);
           }
         } else {
           const u32 k1 = row_k1(q, job.m, lgR);
@@ -261,11 +329,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
 
 template <int LGC, bool SMALL>
 __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
-  switch (blockIdx.y) {
-    case 0: row_body<0, LGC, SMALL>(job, tab, lnr); break;
-    case 1: row_body<1, LGC, SMALL>(job, tab, lnr); break;
-    default: row_body<2, LGC, SMALL>(job, tab, lnr); break;
-  }
+#define PAB_B(P_) row_body<P_, LGC, SMALL>(job, tab, lnr);
+  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+#undef PAB_B
 }
 
 // ---------------------------------------------------------------------------
@@ -283,10 +349,8 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
   constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
-  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
-  const long long kv = op ? job.kX : job.kA;
-  const u32 mask = op ? job.maskX : job.maskA;
-  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
+  const OpView ov = op_view(job, op, b);
+  u32* dst = job.buf + (((long long)b * 2 + op) * job.np + P) * L;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
 
   if constexpr (PP.n == 1) {
@@ -294,18 +358,16 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
       u32 v[1][1 << LGR];
 #pragma unroll
       for (int k = 0; k < (1 << LGR); ++k)
-        v[0][k] = shoup(fetch_word(src, ((long long)k << lgC) + c0 + t, kv, mask), 1u,
-                        PK<P>::one_sh, PK<P>::p);
+        v[0][k] = coef_at<P>(ov, (k << lgC) + c0 + t);
       dif_ct<P, LGR, 1>(v);
 #pragma unroll
       for (int k = 0; k < (1 << LGR); ++k) dst[((long long)k << lgC) + c0 + t] = v[0][k];
     }
   } else {
-    // operand rows >= R/2 are all zero when kv <= L/2 (always for the hash):
+    // operand rows >= R/2 are all zero when kc <= L/2 (always for the hash):
     // skip their loads and turn the first DIF stage into one multiply
-    const bool half = kv <= (L >> 1);
-    const int lim = (int)(kv < L ? kv : L);  // words with index < lim are loaded
-    const int ilast = (int)kv - 1;
+    const bool half = ov.kc <= (L >> 1);
+    const int ilast = ov.kc - 1;
     for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
       const int t = task & (CT - 1), o = task >> lct;
       const int col = c0 + t;
@@ -313,29 +375,20 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
       if (half) {
         const int g0 = (o << lgC) + col;
         constexpr int kTop = ((1 << (RS0 - 1)) - 1) << (SLO0 + lgC);
-        if (g0 + kTop < ilast) {  // every word of the task is valid and unmasked
-          const u32* sp = src + g0;
+        if (g0 + kTop < ilast) {  // every coefficient of the task is valid and unmasked
 #pragma unroll
           for (int k = 0; k < (1 << (RS0 - 1)); ++k)
-            v[0][k] = shoup(__ldg(sp + (k << (SLO0 + lgC))), 1u, PK<P>::one_sh, PK<P>::p);
+            v[0][k] = coef_fast<P>(ov, g0 + (k << (SLO0 + lgC)));
         } else {
 #pragma unroll
-          for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
-            const int gi = g0 + (k << (SLO0 + lgC));
-            u32 w = gi < lim ? __ldg(src + gi) : 0u;
-            w &= gi == ilast ? mask : 0xFFFFFFFFu;
-            v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
-          }
+          for (int k = 0; k < (1 << (RS0 - 1)); ++k)
+            v[0][k] = coef_at<P>(ov, g0 + (k << (SLO0 + lgC)));
         }
         dif_rt_half<P, RS0, SLO0>(v, twf + o);
       } else {
 #pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k) {
-          const int gi = ((o + (k << SLO0)) << lgC) + col;
-          u32 w = gi < lim ? __ldg(src + gi) : 0u;
-          w &= gi == ilast ? mask : 0xFFFFFFFFu;
-          v[0][k] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
-        }
+        for (int k = 0; k < (1 << RS0); ++k)
+          v[0][k] = coef_at<P>(ov, ((o + (k << SLO0)) << lgC) + col);
         dif_rt<P, RS0, SLO0, 1>(v, twf + o);
       }
       const int base = sm_idx(o) * CT + t;
@@ -378,12 +431,12 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int CT = 1 << lct;
-  const int b = blockIdx.z;
+  const int b = blockIdx.y;  // grid (C / CT, batch, prime)
   constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
-  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
-  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
+  const u32* src = job.buf + (((long long)b * 2 + 1) * job.np + P) * L;
+  u32* res = job.buf + (((long long)b * 2 + 0) * job.np + P) * L;
   const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
   const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
 
@@ -498,13 +551,10 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
   constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
-  const u32* src = (op ? job.srcX : job.srcA) + (long long)b * job.src_stride;
-  const long long kv = op ? job.kX : job.kA;
-  const u32 mask = op ? job.maskX : job.maskA;
-  u32* dst = job.buf + (((long long)b * 2 + op) * 3 + P) * L;
+  const OpView ov = op_view(job, op, b);
+  u32* dst = job.buf + (((long long)b * 2 + op) * job.np + P) * L;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
   const uint2* trad = tab.trad + (P * 2 + 0) * tab.tstride;
-  const int lim = (int)(kv < L ? kv : L), ilast = (int)kv - 1;
   constexpr bool FUSE = PP.n >= 2 && M * (1 << PP.rs[0]) <= 32;  // register budget
   if constexpr (FUSE) {
     // radix-M stage fused with the first pow2 pass (when M * 2^RS0 <= 32 values fit in
@@ -522,10 +572,7 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
         u32 a[M];
 #pragma unroll
         for (int s = 0; s < M; ++s) {
-          const int gi = ((j + s * R2) << lgC) + c0 + t;
-          u32 w = gi < lim ? __ldg(src + gi) : 0u;
-          w &= gi == ilast ? mask : 0xFFFFFFFFu;
-          a[s] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+          a[s] = coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
         }
         radix_m<P, M, false>(a);
 #pragma unroll
@@ -551,10 +598,7 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
     u32 a[M];
 #pragma unroll
     for (int s = 0; s < M; ++s) {
-      const int gi = ((j + s * R2) << lgC) + c0 + t;
-      u32 w = gi < lim ? __ldg(src + gi) : 0u;
-      w &= gi == ilast ? mask : 0xFFFFFFFFu;
-      a[s] = shoup(w, 1u, PK<P>::one_sh, PK<P>::p);
+      a[s] = coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
     }
     radix_m<P, M, false>(a);
 #pragma unroll
@@ -595,12 +639,12 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
   constexpr PassPlan PP = pass_plan(LGR2);
   constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
   const int CT = 1 << lct;
-  const int b = blockIdx.z;
+  const int b = blockIdx.y;  // grid (C / CT, batch, prime)
   constexpr int lgC = LGC;
   const long long L = job.L;
   const int c0 = blockIdx.x << lct;
-  const u32* src = job.buf + (((long long)b * 2 + 1) * 3 + P) * L;
-  u32* res = job.buf + (((long long)b * 2 + 0) * 3 + P) * L;
+  const u32* src = job.buf + (((long long)b * 2 + 1) * job.np + P) * L;
+  u32* res = job.buf + (((long long)b * 2 + 0) * job.np + P) * L;
   const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
   const uint2* trad = tab.trad + (P * 2 + 1) * tab.tstride;
   const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
@@ -681,36 +725,28 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
 
 template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(256) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: colm_fwd_body<0, M, LGR2, LGC>(job, tab, lct); break;
-    case 1: colm_fwd_body<1, M, LGR2, LGC>(job, tab, lct); break;
-    default: colm_fwd_body<2, M, LGR2, LGC>(job, tab, lct); break;
-  }
+#define PAB_B(P_) colm_fwd_body<P_, M, LGR2, LGC>(job, tab, lct);
+  PAB_PRIME_SWITCH(PAB_B, blockIdx.y)
+#undef PAB_B
 }
 template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: colm_inv_body<0, M, LGR2, LGC>(job, tab, lct); break;
-    case 1: colm_inv_body<1, M, LGR2, LGC>(job, tab, lct); break;
-    default: colm_inv_body<2, M, LGR2, LGC>(job, tab, lct); break;
-  }
+#define PAB_B(P_) colm_inv_body<P_, M, LGR2, LGC>(job, tab, lct);
+  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+#undef PAB_B
 }
 
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: col_fwd_body<0, LGR, LGC>(job, tab, lct); break;
-    case 1: col_fwd_body<1, LGR, LGC>(job, tab, lct); break;
-    default: col_fwd_body<2, LGR, LGC>(job, tab, lct); break;
-  }
+#define PAB_B(P_) col_fwd_body<P_, LGR, LGC>(job, tab, lct);
+  PAB_PRIME_SWITCH(PAB_B, blockIdx.y)
+#undef PAB_B
 }
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
-  switch (blockIdx.y) {
-    case 0: col_inv_body<0, LGR, LGC>(job, tab, lct); break;
-    case 1: col_inv_body<1, LGR, LGC>(job, tab, lct); break;
-    default: col_inv_body<2, LGR, LGC>(job, tab, lct); break;
-  }
+#define PAB_B(P_) col_inv_body<P_, LGR, LGC>(job, tab, lct);
+  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+#undef PAB_B
 }
 
 

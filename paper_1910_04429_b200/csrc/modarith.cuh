@@ -1,8 +1,9 @@
-// Word-size modular arithmetic for the three-prime NTT (sm_100a integer pipe).
+// Word-size modular arithmetic for the multi-prime NTT (sm_100a integer pipe).
 //
 // The reference multiplies in the Fermat ring Z/(2^N'+1) with shift twiddles
 // (pkg/src/modpa/ntt.py:123-160).  On B200 the product is instead formed as
-// an exact cyclic convolution of 32-bit words over three primes p_i < 2^30
+// an exact cyclic convolution of 64-bit (or 32-bit) coefficients over five
+// (or three) primes p_i < 2^30
 // (CRT-recombined in the carry kernel), so every operation here is on u32
 // registers: Shoup multiplication for known twiddles, Montgomery reduction
 // for products of two data values, and Harvey-style lazy butterflies that
@@ -15,13 +16,20 @@ namespace pab {
 typedef uint32_t u32;
 typedef uint64_t u64;
 
-constexpr int kNumPrimes = 3;
-// p_i < 2^30 (so 4p < 2^32) with 2^22 * 3 * 5 | p_i - 1 (radix-2/3/5 transform
-// lengths); product ~ 2^89.02, so any coefficient K * (2^32-1)^2 with K < 2^25
-// is recovered exactly by CRT.  kGen: a primitive root of each prime.
-constexpr u32 kPrimes[kNumPrimes] = {943718401u, 880803841u, 754974721u};
-constexpr u32 kGen[kNumPrimes] = {7u, 26u, 11u};
-constexpr int kMaxLg = 22;        // 2-adicity common to all three primes
+// Two convolution modes (the "coefficient width" cw of a job):
+//   cw = 2: 64-bit coefficients (two words each) over all five primes; product
+//           ~2^148.85, so K' * (2^64-1)^2 < P for K' <= 1,895,236 coefficients;
+//           lengths m * 2^lg with lg <= kMaxLg5 (n <= 121,295,104 bits).
+//   cw = 1: 32-bit coefficients over the first three primes (2-adicity >= 22),
+//           product ~2^89.02, lengths up to 5 * 2^22 (n <= 335,544,320 bits).
+// Every p_i < 2^30 (so 4p < 2^32) with 3 * 5 | p_i - 1 (radix-3/5 lengths).
+// kGen: a primitive root of each prime.
+constexpr int kNumPrimes = 5;
+constexpr u32 kPrimes[kNumPrimes] = {943718401u, 880803841u, 754974721u, 1053818881u,
+                                     975175681u};
+constexpr u32 kGen[kNumPrimes] = {7u, 26u, 11u, 7u, 17u};
+constexpr int kMaxLg = 22;        // 2-adicity common to primes 0..2 (cw = 1)
+constexpr int kMaxLg5 = 20;       // 2-adicity common to all five (cw = 2)
 constexpr int kTwN = 4096;        // largest in-CTA sub-transform
 constexpr int kTwLg = 12;
 

@@ -53,6 +53,8 @@ struct PK {
   static constexpr u32 two_p = 2u * kPrimes[P];
   static constexpr u32 p_mont = cmont_neg_inv(kPrimes[P]);
   static constexpr u32 one_sh = cshoup(1u, kPrimes[P]);
+  static constexpr u32 r32 = (u32)((1ull << 32) % kPrimes[P]);  // 2^32 mod p
+  static constexpr u32 r32_sh = cshoup(r32, kPrimes[P]);
 };
 
 // ------------------------------------------------------------ static for

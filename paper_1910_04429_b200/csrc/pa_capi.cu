@@ -4,13 +4,16 @@
 // pa_round pa.py:193-217 (validation stays in Python), mul bignum.py:194-231,
 // fused_mul_add bignum.py:234-238, import/export layout pa.py:111-132.
 // The reference's SSA plan (ntt.py:69-108) chooses a Fermat-ring geometry;
-// here the plan is the transform length L = 2^lg >= 2*ceil(n/32) - 1 of a
-// three-prime word convolution and its four-step split L = R * C.
+// here the plan is the coefficient width (64-bit coefficients over five
+// primes, or 32-bit over three for the largest blocks), the transform length
+// L = m * 2^lg >= 2 K' - 1 (K' coefficients per operand) and its four-step
+// split L = R * C.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -31,7 +34,8 @@ using namespace pab;
 namespace {
 
 thread_local std::string g_err;
-constexpr int kTw4MaxLg = 20;  // full four-step twiddle tables up to L = 2^20 (48 L bytes <= 48 MiB)
+std::atomic<int> g_force_cw{0};  // test hook (pab_force_coef_words): 0 = automatic
+constexpr int kTw4MaxLg = 20;  // full four-step twiddle tables up to L = 2^20 (80 L bytes <= 80 MiB)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -81,9 +85,9 @@ struct Geo {
   u64 L = 0;
 };
 
-// Cheapest length >= need among m * 2^lg, m in {1, 3, 5} (radix-3/5 column
-// stage costs ~2.5 / ~3.7 radix-2 stages).  Returns false if none fits.
-bool choose_geo(u64 need, Geo* out) {
+// Cheapest length >= need among m * 2^lg (lg <= maxlg), m in {1, 3, 5} (radix-3/5
+// column stage costs ~2.5 / ~3.7 radix-2 stages).  Returns false if none fits.
+bool choose_geo(u64 need, int maxlg, Geo* out) {
   Geo best;
   double best_cost = 0;
   bool found = false;
@@ -93,7 +97,7 @@ bool choose_geo(u64 need, Geo* out) {
     const int m = ms[i];
     int lg = 0;
     while (((u64)m << lg) < need || ((u64)m << lg) < 64) ++lg;
-    if (lg > kMaxLg) continue;
+    if (lg > maxlg) continue;
     Geo g;
     g.m = m;
     g.lg = lg;
@@ -174,22 +178,10 @@ int ensure_device(int dev, DevState** out) {
       for (int j = 0; q[j]; ++j)
         if ((p - 1) % q[j] != 0 || powmod(kGen[i], (p - 1) / q[j], p) == 1)
           return fail(PAB_ECUDA, "internal: bad prime / generator constants");
-      if (((p - 1) >> kMaxLg) << kMaxLg != p - 1)
+      const int need = i < 3 ? kMaxLg : kMaxLg5;
+      if (((p - 1) >> need) << need != p - 1)
         return fail(PAB_ECUDA, "internal: prime 2-adicity below kMaxLg");
     }
-    CrtConst crt;
-    crt.p0 = kPrimes[0];
-    crt.p1 = kPrimes[1];
-    crt.p2 = kPrimes[2];
-    crt.inv01 = inv_mod(crt.p0 % crt.p1, crt.p1);
-    crt.inv01_sh = shoup_of(crt.inv01, crt.p1);
-    crt.p0m2 = crt.p0 % crt.p2;
-    crt.p0m2_sh = shoup_of(crt.p0m2, crt.p2);
-    crt.inv012 = inv_mod((u32)(((u64)crt.p0 * crt.p1) % crt.p2), crt.p2);
-    crt.inv012_sh = shoup_of(crt.inv012, crt.p2);
-    crt.p0p1 = (u64)crt.p0 * crt.p1;
-    upload_constants(crt);
-    CK(cudaGetLastError(), "upload constants");
     // stage twiddles tw[h + e] = w_{2h}^{+-e}
     std::vector<uint2> stw((size_t)kNumPrimes * 2 * kTwN);
     for (int i = 0; i < kNumPrimes; ++i) {
@@ -259,6 +251,8 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   const int slo0 = pass_plan(geo.lgC).slo[0];
   for (int i = 0; i < kNumPrimes; ++i) {
     const u32 p = kPrimes[i];
+    pl.scale[i] = pl.scale_sh[i] = 0;
+    if ((p - 1) % L != 0) continue;  // a cw = 1 length beyond this prime's 2-adicity
     const u64 r32 = ((u64)1 << 32) % p;
     for (int dir = 0; dir < 2; ++dir) {
       const size_t pd = (size_t)i * 2 + dir;
@@ -295,11 +289,12 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   if ((rc = upload((void**)&pl.thi, thi.data(), thi.size() * sizeof(uint2)))) return rc;
   if ((rc = upload((void**)&pl.g, gt.data(), gt.size() * sizeof(uint2)))) return rc;
   if ((rc = upload((void**)&pl.trad, trad.data(), trad.size() * sizeof(uint2)))) return rc;
-  // full four-step twiddle tables (L <= 2^kTw4MaxLg): 48 L bytes, read once per launch
+  // full four-step twiddle tables (L <= 2^kTw4MaxLg): 80 L bytes, read once per launch
   if (R > 1 && L <= ((u64)1 << kTw4MaxLg)) {
     std::vector<uint2> t4((size_t)kNumPrimes * 2 * L);
     for (int i = 0; i < kNumPrimes; ++i) {
       const u32 p = kPrimes[i];
+      if ((p - 1) % L != 0) continue;
       for (int dir = 0; dir < 2; ++dir) {
         const u32 wL = root_of(i, L, dir);
         uint2* t = &t4[((size_t)i * 2 + dir) * L];
@@ -339,11 +334,61 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   return t;
 }
 
-// exact three-prime convolution: k * (2^32-1)^2 < P = p0 p1 p2
-bool crt_bound_ok(u64 k) {
-  unsigned __int128 P = (unsigned __int128)kPrimes[0] * kPrimes[1] * kPrimes[2];
-  unsigned __int128 w = (unsigned __int128)0xFFFFFFFFu * 0xFFFFFFFFu;
-  return (unsigned __int128)k * w < P;
+// Exact convolution bound: k coefficients of cw words each give coefficient
+// sums below k * (2^(32 cw) - 1)^2, which must stay below P = p_0 ... p_(np-1).
+// Multiword (3 x 64-bit limbs, P < 2^150).
+void limbs_mul(u64 a[3], u64 m) {
+  unsigned __int128 c = 0;
+  for (int i = 0; i < 3; ++i) {
+    c += (unsigned __int128)a[i] * m;
+    a[i] = (u64)c;
+    c >>= 64;
+  }
+}
+bool limbs_lt(const u64 a[3], const u64 b[3]) {
+  for (int i = 2; i >= 0; --i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return false;
+}
+bool crt_bound_ok(u64 k, int cw) {
+  const int np = cw == 2 ? 5 : 3;
+  u64 P[3] = {1, 0, 0};
+  for (int i = 0; i < np; ++i) limbs_mul(P, kPrimes[i]);
+  // (2^(32 cw) - 1)^2 as limbs
+  u64 X[3];
+  if (cw == 2) {  // 2^128 - 2^65 + 1
+    X[0] = 1;
+    X[1] = 0xFFFFFFFFFFFFFFFEull;
+    X[2] = 0;
+  } else {
+    X[0] = 0xFFFFFFFE00000001ull;
+    X[1] = X[2] = 0;
+  }
+  limbs_mul(X, k);
+  return limbs_lt(X, P);
+}
+
+// Convolution mode: coefficient words (2: five primes, 1: three primes).
+struct Mode {
+  int cw = 1, np = 3;
+  Geo geo;
+};
+
+// product of two operands of ka and kb words: prefer 64-bit coefficients
+bool choose_mode(u64 ka, u64 kb, Mode* md) {
+  const int force = g_force_cw.load();
+  const u64 ca = (ka + 1) / 2, cb = (kb + 1) / 2;
+  if (force != 1 && crt_bound_ok(ca < cb ? ca : cb, 2) && choose_geo(ca + cb - 1, kMaxLg5, &md->geo)) {
+    md->cw = 2;
+    md->np = 5;
+    return true;
+  }
+  if (force != 2 && crt_bound_ok(ka < kb ? ka : kb, 1) && choose_geo(ka + kb - 1, kMaxLg, &md->geo)) {
+    md->cw = 1;
+    md->np = 3;
+    return true;
+  }
+  return false;
 }
 
 constexpr u64 kMaxChunk = 16384;  // blocks per launch (grid.y/z <= 65535)
@@ -360,7 +405,7 @@ struct Layout {
   size_t off_words, off_buf, off_out, off_state, off_ctr, total;
 };
 
-Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch) {
+Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch, int np) {
   Layout ly;
   ly.in_stride = round_up(kmax > 0 ? kmax : 1, 64);
   ly.L = L;
@@ -373,7 +418,7 @@ Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch) {
     return o;
   };
   ly.off_words = take(batch * 3 * ly.in_stride * 4);
-  ly.off_buf = take(batch * 6 * ly.L * 4);
+  ly.off_buf = take(batch * 2 * np * ly.L * 4);
   ly.off_out = take(batch * mw * 4);
   ly.off_state = take(batch * ly.tiles * 8);
   ly.off_ctr = take(batch * 4);
@@ -383,7 +428,8 @@ Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch) {
 
 struct HashGeo {
   u64 K;    // words per operand
-  Geo geo;
+  Mode md;
+  u64 KC;   // coefficients per operand (K / cw rounded up)
   u64 mw;
 };
 
@@ -392,17 +438,21 @@ int hash_geo(u64 n, u64 r, HashGeo* g) {
   if (r < 1 || r > n) return fail(PAB_EINVAL, "output length r must satisfy 1 <= r <= n");
   if (n > pab_max_bits()) return fail(PAB_ERANGE, "block length exceeds pab_max_bits()");
   g->K = ceil_div(n, 32);
-  if (!choose_geo(2 * g->K - 1, &g->geo))
+  if (!choose_mode(g->K, g->K, &g->md))
     return fail(PAB_ERANGE, "no transform geometry for this block length");
+  g->KC = ceil_div(g->K, (u64)g->md.cw);
   g->mw = ceil_div(r, 32);
   return PAB_OK;
 }
 
-ConvJob make_job(const Layout& ly, void* ws, const Geo& geo, int batch) {
+ConvJob make_job(const Layout& ly, void* ws, const Mode& md, int batch) {
+  const Geo& geo = md.geo;
   ConvJob j;
   std::memset(&j, 0, sizeof(j));
   char* base = (char*)ws;
   j.batch = batch;
+  j.cw = md.cw;
+  j.np = md.np;
   j.m = geo.m;
   j.lg = geo.lg;
   j.lgR = geo.lgR;
@@ -418,7 +468,7 @@ ConvJob make_job(const Layout& ly, void* ws, const Geo& geo, int batch) {
   return j;
 }
 
-bool aligned4(const void* p) { return ((uintptr_t)p & 3) == 0; }
+bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)) == 0; }
 
 }  // namespace
 
@@ -436,18 +486,29 @@ int pab_plan_info(uint64_t n_bits, int* radix, int* lg, int* lg_rows, int* lg_co
   HashGeo g;
   int rc = hash_geo(n_bits, 1, &g);
   if (rc) return rc;
-  if (radix) *radix = g.geo.m;
-  if (lg) *lg = g.geo.lg;
-  if (lg_rows) *lg_rows = g.geo.lgR;
-  if (lg_cols) *lg_cols = g.geo.lgC;
+  if (radix) *radix = g.md.geo.m;
+  if (lg) *lg = g.md.geo.lg;
+  if (lg_rows) *lg_rows = g.md.geo.lgR;
+  if (lg_cols) *lg_cols = g.md.geo.lgC;
   return PAB_OK;
 }
+
+int pab_plan_width(uint64_t n_bits, int* coef_bits, int* primes) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, 1, &g);
+  if (rc) return rc;
+  if (coef_bits) *coef_bits = 32 * g.md.cw;
+  if (primes) *primes = g.md.np;
+  return PAB_OK;
+}
+
+void pab_force_coef_words(int cw) { g_force_cw.store(cw == 1 || cw == 2 ? cw : 0); }
 
 size_t pab_hash_workspace_bytes(uint64_t n_bits, uint32_t batch) {
   HashGeo g;
   if (hash_geo(n_bits, 1, &g)) return 0;
   // output words are bounded by K; size for the largest r
-  return layout_for(g.K, g.geo.L, g.K, g.K, batch ? batch : 1).total;
+  return layout_for(g.K, g.md.geo.L, g.K, g.K, batch ? batch : 1, g.md.np).total;
 }
 
 int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t in_stride,
@@ -467,27 +528,30 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   DevState* ds;
   if ((rc = current_device(&ds))) return rc;
   const Plan* pl;
-  if ((rc = get_plan(ds, g.geo, &pl))) return rc;
+  if ((rc = get_plan(ds, g.md.geo, &pl))) return rc;
   const PlanTables tab = tables_of(ds, pl);
   cudaStream_t st = (cudaStream_t)stream;
   // blocks per chunk that fit the workspace
   u64 chunk = batch < kMaxChunk ? batch : kMaxChunk;  // grid y/z limits
-  while (chunk > 0 && layout_for(g.K, g.geo.L, g.K, g.mw, chunk).total > workspace_bytes) chunk /= 2;
+  while (chunk > 0 && layout_for(g.K, g.md.geo.L, g.K, g.mw, chunk, g.md.np).total > workspace_bytes)
+    chunk /= 2;
   if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
   const int msf = byte_order == PAB_ORDER_MSF;
   // LSF blocks whose words can be read in place (the common case): no pack kernel
-  const bool direct_in = !msf && nbytes % 4 == 0 && in_stride % 4 == 0 && aligned4(x) &&
-                         aligned4(c) && aligned4(d);
-  const bool direct_out = !msf && out_stride % 4 == 0 && aligned4(out);
+  // (64-bit coefficients are read as 8-byte words: whole, 8-byte aligned rows)
+  const u64 al = 4 * (u64)g.md.cw;
+  const bool direct_in = !msf && nbytes % al == 0 && in_stride % al == 0 && aligned(x, al) &&
+                         aligned(c, al) && aligned(d, al);
+  const bool direct_out = !msf && out_stride % 4 == 0 && aligned(out, 4);
   const u32 mask = (n_bits & 31) ? ((1u << (n_bits & 31)) - 1u) : 0xFFFFFFFFu;
   for (u64 b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = (int)((batch - b0) < chunk ? (batch - b0) : chunk);
-    const Layout ly = layout_for(g.K, g.geo.L, g.K, g.mw, nb);
-    ConvJob job = make_job(ly, workspace, g.geo, nb);
+    const Layout ly = layout_for(g.K, g.md.geo.L, g.K, g.mw, nb, g.md.np);
+    ConvJob job = make_job(ly, workspace, g.md, nb);
     job.kA = job.kX = job.kD = (long long)g.K;
     job.maskA = job.maskX = job.maskD = mask;
     job.nT = (long long)g.K;
-    job.nRes = (long long)g.K;
+    job.nRes = (long long)g.KC;
     job.n_mod_bits = (long long)n_bits;
     job.shift = (long long)(n_bits - r_bits);
     job.mw = (long long)g.mw;
@@ -613,9 +677,9 @@ size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes) {
   const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4);
   if (ka == 0 || kb == 0) return 256;
   const u64 nT = ka + kb;
-  Geo geo;
-  if (!choose_geo(ka + kb - 1, &geo)) return 0;
-  return layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1).total;
+  Mode md;
+  if (!choose_mode(ka, kb, &md)) return 0;
+  return layout_for(ka > kb ? ka : kb, md.geo.L, nT, nT, 1, md.np).total;
 }
 
 int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes, uint8_t* out,
@@ -628,22 +692,24 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
     return PAB_OK;
   }
   const u64 nT = ka + kb;
-  Geo geo;
-  if (!choose_geo(ka + kb - 1, &geo) || !crt_bound_ok(ka < kb ? ka : kb))
-    return fail(PAB_ERANGE, "operands exceed the exact three-prime convolution range");
-  const Layout ly = layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1);
+  Mode md;
+  if (!choose_mode(ka, kb, &md))
+    return fail(PAB_ERANGE, "operands exceed the exact multi-prime convolution range");
+  const Geo& geo = md.geo;
+  const Layout ly = layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1, md.np);
   if (workspace_bytes < ly.total) return fail(PAB_EINVAL, "workspace too small");
   int rc;
   DevState* ds;
   if ((rc = current_device(&ds))) return rc;
   const Plan* pl;
   if ((rc = get_plan(ds, geo, &pl))) return rc;
-  ConvJob job = make_job(ly, workspace, geo, 1);
+  ConvJob job = make_job(ly, workspace, md, 1);
   job.kA = (long long)ka;
   job.kX = (long long)kb;
   job.kD = 0;
   job.nT = (long long)nT;
-  job.nRes = (long long)(nT < ly.L ? nT : ly.L);
+  // product coefficients 0 .. ca + cb - 2 (<= L - 1)
+  job.nRes = (long long)(ceil_div(ka, (u64)md.cw) + ceil_div(kb, (u64)md.cw) - 1);
   job.n_mod_bits = 32ll * (long long)nT;
   job.shift = 0;
   job.mw = (long long)nT;

@@ -15,6 +15,7 @@
 //              export_block pa.py:128-132)
 //   k_pack / k_unpack  only for MSF or unaligned layouts.
 // For L <= 4096 a single k_row CTA per (block, prime) does the whole transform.
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -97,10 +98,6 @@ int profile_collect(const char** names, int* counts, double* ms, int cap) {
   return nn;
 }
 
-__constant__ CrtConst c_crt;
-
-void upload_constants(const CrtConst& crt) { cudaMemcpyToSymbol(c_crt, &crt, sizeof(CrtConst)); }
-
 // ---------------------------------------------------------------------------
 // pack / unpack (MSF byte order or unaligned blocks only)
 
@@ -167,8 +164,8 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
 }
 
 // ---------------------------------------------------------------------------
-// Carry: CRT of the three residues, overlap-add of the 96-bit coefficients at
-// 32-bit stride, + D, carry-lookahead scan (decoupled look-back across tiles),
+// Carry: CRT of the residues, overlap-add of the 160-bit (cw = 2) or 96-bit
+// (cw = 1) coefficients at 64/32-bit stride, + D, carry-lookahead scan (decoupled look-back across tiles),
 // mask to n_mod_bits, shift right, write the key.
 
 struct CarryFn {  // c -> q + (c >= t); id marks the identity
@@ -190,31 +187,250 @@ __device__ __forceinline__ u32 cf_apply(CarryFn f, u32 c) {
   return f.id ? c : f.q + (c >= f.t ? 1u : 0u);
 }
 
-__device__ __forceinline__ void crt3(u32 r0, u32 r1, u32 r2, u32& w0, u32& w1, u32& w2) {
-  const CrtConst& k = c_crt;
-  const u32 v0 = r0;
-  const u32 x1 = r1 + 2u * k.p1 - v0;
-  const u32 v1 = red(shoup(x1, k.inv01, k.inv01_sh, k.p1), k.p1);
-  u32 u = v0 + shoup(v1, k.p0m2, k.p0m2_sh, k.p2);  // [0, 4 p2)
-  u = red(u, 2u * k.p2);
-  const u32 x2 = r2 + 2u * k.p2 - u;
-  const u32 v2 = red(shoup(x2, k.inv012, k.inv012_sh, k.p2), k.p2);
-  const u64 lo = (u64)v0 + (u64)k.p0 * v1;  // < 2^61
-  const u64 prod_lo = k.p0p1 * (u64)v2;
-  u64 prod_hi = __umul64hi(k.p0p1, (u64)v2);
-  const u64 s = lo + prod_lo;
-  prod_hi += (s < lo) ? 1ull : 0ull;
-  w0 = (u32)s;
-  w1 = (u32)(s >> 32);
-  w2 = (u32)prod_hi;
+// CRT by Garner's mixed radix, all constants compile-time (SASS immediates):
+// v_0 = r_0, v_i = (...((r_i - v_0) p_0^-1 - v_1) p_1^-1 ... - v_{i-1}) p_{i-1}^-1 mod p_i,
+// x = v_0 + p_0 (v_1 + p_1 (v_2 + ...)).  Lazy values stay in [0, 2 p_i).
+template <int I, int J>
+struct Garner {  // p_J^-1 mod p_I with its Shoup companion
+  static constexpr u32 w = cpow(kPrimes[J] % kPrimes[I], kPrimes[I] - 2, kPrimes[I]);
+  static constexpr u32 wp = cshoup(w, kPrimes[I]);
+};
+
+template <int NP>
+__device__ __forceinline__ void garner(const u32 (&r)[NP], u32 (&v)[NP]) {
+  v[0] = r[0];
+  sfor<NP - 1>([&](auto im1) {
+    constexpr int I = decltype(im1)::value + 1;
+    constexpr u32 p = kPrimes[I];
+    u32 t = r[I];
+    sfor<I>([&](auto jc) {
+      constexpr int J = decltype(jc)::value;
+      t = shoup(t + 2u * p - v[J], Garner<I, J>::w, Garner<I, J>::wp, p);  // 2p > v_J
+    });
+    v[I] = red(t, p);
+  });
 }
 
-__device__ __forceinline__ void crt_at(const u32* r0, const u32* r1, const u32* r2, long long k,
-                                       long long nres, u32& w0, u32& w1, u32& w2) {
-  if (k >= 0 && k < nres) {
-    crt3(__ldg(r0 + k), __ldg(r1 + k), __ldg(r2 + k), w0, w1, w2);
-  } else {
-    w0 = w1 = w2 = 0u;
+// Mixed-radix reconstruction x = v0 + p0 (v1 + p1 (v2 + ...)) in 32-bit limbs:
+// every step is limb * p + (addend) < 2^62, one IMAD.WIDE.U32 each.
+// three primes (cw = 1): x < 2^90 -> 3 words
+__device__ __forceinline__ void crt3(u32 r0, u32 r1, u32 r2, u32& w0, u32& w1, u32& w2) {
+  const u32 r[3] = {r0, r1, r2};
+  u32 v[3];
+  garner<3>(r, v);
+  constexpr u32 p0 = kPrimes[0], p1 = kPrimes[1];
+  u64 t = (u64)v[2] * p1 + v[1];  // < 2^60
+  const u32 a0 = (u32)t, a1 = (u32)(t >> 32);
+  t = (u64)a0 * p0 + v[0];
+  w0 = (u32)t;
+  t = (u64)a1 * p0 + (t >> 32);
+  w1 = (u32)t;
+  w2 = (u32)(t >> 32);
+}
+
+// five primes (cw = 2): x < 2^149 -> 5 words
+__device__ __forceinline__ void crt5(const u32 (&r)[5], u32 (&w)[5]) {
+  u32 v[5];
+  garner<5>(r, v);
+  constexpr u32 p0 = kPrimes[0], p1 = kPrimes[1], p2 = kPrimes[2], p3 = kPrimes[3];
+  u64 t = (u64)v[4] * p3 + v[3];  // a = v3 + p3 v4 < 2^60
+  const u32 a0 = (u32)t, a1 = (u32)(t >> 32);
+  t = (u64)a0 * p2 + v[2];  // b = v2 + p2 a < 2^90
+  const u32 b0 = (u32)t;
+  t = (u64)a1 * p2 + (t >> 32);
+  const u32 b1 = (u32)t, b2 = (u32)(t >> 32);
+  t = (u64)b0 * p1 + v[1];  // c = v1 + p1 b < 2^120
+  const u32 c0 = (u32)t;
+  t = (u64)b1 * p1 + (t >> 32);
+  const u32 c1 = (u32)t;
+  t = (u64)b2 * p1 + (t >> 32);
+  const u32 c2 = (u32)t, c3 = (u32)(t >> 32);
+  t = (u64)c0 * p0 + v[0];  // x = v0 + p0 c < 2^150
+  w[0] = (u32)t;
+  t = (u64)c1 * p0 + (t >> 32);
+  w[1] = (u32)t;
+  t = (u64)c2 * p0 + (t >> 32);
+  w[2] = (u32)t;
+  t = (u64)c3 * p0 + (t >> 32);
+  w[3] = (u32)t;
+  w[4] = (u32)(t >> 32);
+}
+
+__device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long gi, long long kv,
+                                          u32 mask) {
+  if (gi >= kv) return 0u;
+  const u32 w = __ldg(src + gi);
+  return gi == kv - 1 ? (w & mask) : w;
+}
+
+struct CarrySmem {
+  u32 tile, cin;
+  u32 wq[kCarryWarps], wt[kCarryWarps];
+  u32 first[kCarryWarps];
+  // cw = 2: high words of each warp's top two coefficients for the warp above
+  // (w2, w3 of lane 31, w4 of lanes 30 and 31), double-buffered by tile parity
+  u32 nb[2][kCarryWarps][4];
+};
+
+// Column sums of one warp's kCarryRows x 32 words starting at word wb:
+// S[i] (lane j) = sum of the CRT'd coefficient words landing on word wb + 32 i + j.
+// s_next (warp-uniform `last` only): the same sum for word wb + 32 kCarryRows.
+//
+// cw = 1: coefficient k (3 words) lands on words k, k+1, k+2.
+__device__ __forceinline__ void sums_cw1(const u32* __restrict__ res, long long L, long long nres,
+                                         long long wb, bool last, u64 (&S)[kCarryRows],
+                                         u64& s_next) {
+  constexpr int NR = kCarryRows;
+  const int lane = threadIdx.x & 31;
+  const u32* res0 = res;
+  const u32* res1 = res + L;
+  const u32* res2 = res + 2 * L;
+  // issue every load first (memory-level parallelism), then CRT
+  u32 V0[NR], V1[NR], V2[NR];
+  const bool in_res = wb + NR * 32 <= nres;
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const long long k = wb + i * 32 + lane;
+    const bool ok = in_res || k < nres;
+    V0[i] = ok ? __ldg(res0 + k) : 0u;
+    V1[i] = ok ? __ldg(res1 + k) : 0u;
+    V2[i] = ok ? __ldg(res2 + k) : 0u;
+  }
+  // virtual row -1 (lanes 30, 31 hold coefficients wb-2, wb-1)
+  u32 P1 = 0, P2 = 0;
+  {
+    const long long k = wb - 32 + lane;
+    const bool ok = lane >= 30 && k >= 0 && k < nres;
+    const u32 q0 = ok ? __ldg(res0 + k) : 0u, q1 = ok ? __ldg(res1 + k) : 0u,
+              q2 = ok ? __ldg(res2 + k) : 0u;
+    u32 x0;
+    crt3(q0, q1, q2, x0, P1, P2);
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) crt3(V0[i], V1[i], V2[i], V0[i], V1[i], V2[i]);
+  // S_k = V0[k] + V1[k-1] + V2[k-2]  (zero residues CRT to zero)
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const u32 p1row = i ? V1[i - 1] : P1, p2row = i ? V2[i - 1] : P2;
+    const u32 a1 = __shfl_up_sync(0xFFFFFFFFu, V1[i], 1);
+    const u32 b1 = __shfl_sync(0xFFFFFFFFu, p1row, 31);
+    const u32 a2 = __shfl_up_sync(0xFFFFFFFFu, V2[i], 2);
+    const u32 b2 = __shfl_sync(0xFFFFFFFFu, p2row, 30 + (lane & 1));
+    S[i] = (u64)V0[i] + (lane ? a1 : b1) + (lane >= 2 ? a2 : b2);
+  }
+  if (last) {
+    const long long k = wb + NR * 32;
+    u32 n0 = 0, n1, n2;
+    if (lane == 0 && k < nres) crt3(__ldg(res0 + k), __ldg(res1 + k), __ldg(res2 + k), n0, n1, n2);
+    n0 = __shfl_sync(0xFFFFFFFFu, n0, 0);
+    const u32 v1 = __shfl_sync(0xFFFFFFFFu, V1[NR - 1], 31);
+    const u32 v2 = __shfl_sync(0xFFFFFFFFu, V2[NR - 1], 30);
+    s_next = (u64)n0 + v1 + v2;
+  }
+}
+
+// cw = 2: coefficient c (5 words) lands on words 2c .. 2c+4, so even word 2c
+// sums w0(c) + w2(c-1) + w4(c-2) and odd word 2c+1 sums w1(c) + w3(c-1).
+// A pair of rows (64 words) is 32 coefficients: lane j CRTs coefficient
+// cb + 32 q + j, then shuffles route the words.  In the sequential mode the
+// two coefficients below a warp come from the warp beneath through shared
+// memory (the previous tile's top warp for warp 0; contains a __syncthreads);
+// in the look-back mode each warp recomputes them.
+template <bool LOOKBACK>
+__device__ __forceinline__ void sums_cw2(const u32* __restrict__ res, long long L, long long nres,
+                                         long long wb, int tile, CarrySmem& sm,
+                                         u64 (&S)[kCarryRows], u64& s_next) {
+  constexpr int NQ = kCarryRows / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool last = warp == kCarryWarps - 1;
+  const long long cb = wb >> 1;
+  u32 W[NQ][5];
+  const bool in_res = cb + NQ * 32 <= nres;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const long long k = cb + q * 32 + lane;
+    const bool ok = in_res || k < nres;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) W[q][i] = ok ? __ldg(res + i * L + k) : 0u;
+  }
+  u32 nx[5] = {0u, 0u, 0u, 0u, 0u};  // top warp: the next tile's first coefficient (lane 0)
+  const long long kn = cb + NQ * 32;
+  if (last && lane == 0 && kn < nres) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) nx[i] = __ldg(res + i * L + kn);
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) crt5(W[q], W[q]);
+  if (last && lane == 0 && kn < nres) crt5(nx, nx);
+  // w2(c-1), w3(c-1) from lane 31 and w4(c-2) from lanes 30 / 31 of the pair below
+  u32 pw2 = 0, pw3 = 0, pw4a = 0, pw4b = 0;
+  if constexpr (LOOKBACK) {  // every warp recomputes them (no barrier: warps stay independent)
+    const long long k = cb - 32 + lane;
+    const bool ok = lane >= 30 && k >= 0 && k < nres;
+    u32 Pv[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) Pv[i] = ok ? __ldg(res + i * L + k) : 0u;
+    crt5(Pv, Pv);
+    pw2 = __shfl_sync(0xFFFFFFFFu, Pv[2], 31);
+    pw3 = __shfl_sync(0xFFFFFFFFu, Pv[3], 31);
+    pw4a = __shfl_sync(0xFFFFFFFFu, Pv[4], 30);
+    pw4b = __shfl_sync(0xFFFFFFFFu, Pv[4], 31);
+  } else {  // from the warp beneath (the previous tile's top warp for warp 0)
+    if (lane >= 30) {
+      u32* nb = sm.nb[tile & 1][warp];
+      if (lane == 31) {
+        nb[0] = W[NQ - 1][2];
+        nb[1] = W[NQ - 1][3];
+        nb[3] = W[NQ - 1][4];
+      } else {
+        nb[2] = W[NQ - 1][4];
+      }
+    }
+    __syncthreads();
+    if (warp > 0 || tile > 0) {
+      const u32* nb = warp ? sm.nb[tile & 1][warp - 1] : sm.nb[(tile - 1) & 1][kCarryWarps - 1];
+      pw2 = nb[0];
+      pw3 = nb[1];
+      pw4a = nb[2];
+      pw4b = nb[3];
+    }
+  }
+  const bool odd = lane & 1;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int sl = 16 * h + (lane >> 1);  // source lane of coefficient c
+      const u32 x0 = __shfl_sync(0xFFFFFFFFu, W[q][0], sl);
+      const u32 x1 = __shfl_sync(0xFFFFFFFFu, W[q][1], sl);
+      u32 y2 = __shfl_sync(0xFFFFFFFFu, W[q][2], (sl - 1) & 31);
+      u32 y3 = __shfl_sync(0xFFFFFFFFu, W[q][3], (sl - 1) & 31);
+      u32 z4 = __shfl_sync(0xFFFFFFFFu, W[q][4], (sl - 2) & 31);
+      if (h == 0) {  // c-1 / c-2 below this pair: lanes 31 / 30 + sl of the previous one
+        u32 py2, py3, pz4;
+        if (q == 0) {
+          py2 = pw2;
+          py3 = pw3;
+          pz4 = sl == 0 ? pw4a : pw4b;
+        } else {
+          py2 = __shfl_sync(0xFFFFFFFFu, W[q - 1][2], 31);
+          py3 = __shfl_sync(0xFFFFFFFFu, W[q - 1][3], 31);
+          pz4 = __shfl_sync(0xFFFFFFFFu, W[q - 1][4], (30 + sl) & 31);
+        }
+        if (sl == 0) {
+          y2 = py2;
+          y3 = py3;
+        }
+        if (sl < 2) z4 = pz4;
+      }
+      S[2 * q + h] = odd ? (u64)x1 + y3 : (u64)x0 + y2 + z4;
+    }
+  }
+  if (last) {  // word wb + 32 NR = 2 kn: w0(kn) + w2(kn - 1) + w4(kn - 2)
+    const u32 n0 = __shfl_sync(0xFFFFFFFFu, nx[0], 0);
+    const u32 v2 = __shfl_sync(0xFFFFFFFFu, W[NQ - 1][2], 31);
+    const u32 v4 = __shfl_sync(0xFFFFFFFFu, W[NQ - 1][4], 30);
+    s_next = (u64)n0 + v2 + v4;
   }
 }
 
@@ -226,11 +442,6 @@ __device__ __forceinline__ void crt_at(const u32* r0, const u32* r1, const u32* 
 // P = ballot(word == ~0), the carries into all lanes are (A+B)^A^B for
 // A = G|P, B = G.  Rows chain sequentially inside the warp; warps and tiles
 // compose carry functions c -> q + (c >= t).
-struct CarrySmem {
-  u32 tile, cin;
-  u32 wq[kCarryWarps], wt[kCarryWarps];
-  u32 first[kCarryWarps];
-};
 
 // Resolve one row: s = column sums (u64) of this lane's word, cin_row = carry
 // into lane 0 (< 2^32).  Returns final word; updates cin_row to the row's
@@ -257,100 +468,51 @@ __device__ __forceinline__ u32 carry_row(u64 s, u32& cin_row, unsigned& ones_mas
 
 // One tile of block b; LOOKBACK: carry-in via decoupled look-back, else cin_seq.
 // Returns the carry out of the tile.
-template <bool LOOKBACK>
+template <bool LOOKBACK, int CW>
 __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int b, int tile,
                                           u32 cin_seq) {
   constexpr int NR = kCarryRows;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long L = job.L;
-  const u32* res0 = job.buf + (((long long)b * 2 + 0) * 3 + 0) * L;
-  const u32* res1 = res0 + L;
-  const u32* res2 = res1 + L;
+  const u32* res = job.buf + (long long)b * 2 * job.np * L;  // prime i at res + i * L
   const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
   const long long tbase = (long long)tile * kCarryTile;
   const long long wb = tbase + (long long)warp * NR * 32;  // first word of this warp
-  const long long nres = job.nRes;
+  const bool last = warp == kCarryWarps - 1;
 
-  // issue every load of the tile first (memory-level parallelism), then CRT.
-  // Warps entirely inside the valid ranges skip all per-word bounds checks.
-  u32 V0[NR], V1[NR], V2[NR], DV[NR];
+  u32 DV[NR];
   const long long kd = dw ? job.kD : 0;
-  const bool in_res = wb + NR * 32 <= nres;
-  const bool in_d = wb + NR * 32 < kd;
-  if (in_res) {
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const long long k = wb + i * 32 + lane;
-      V0[i] = __ldg(res0 + k);
-      V1[i] = __ldg(res1 + k);
-      V2[i] = __ldg(res2 + k);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const long long k = wb + i * 32 + lane;
-      const bool ok = k < nres;
-      V0[i] = ok ? __ldg(res0 + k) : 0u;
-      V1[i] = ok ? __ldg(res1 + k) : 0u;
-      V2[i] = ok ? __ldg(res2 + k) : 0u;
-    }
-  }
-  if (in_d) {
+  if (wb + NR * 32 < kd) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) DV[i] = __ldg(dw + wb + i * 32 + lane);
   } else {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const long long k = wb + i * 32 + lane;
-      DV[i] = k < kd ? __ldg(dw + k) : 0u;
-      if (k == kd - 1) DV[i] &= job.maskD;
-    }
+    for (int i = 0; i < NR; ++i) DV[i] = fetch_word(dw, wb + i * 32 + lane, kd, job.maskD);
   }
-  // virtual row -1 (lanes 30, 31 hold coefficients wb-2, wb-1)
-  u32 P1 = 0, P2 = 0;
-  {
-    const long long k = wb - 32 + lane;
-    const bool ok = lane >= 30 && k >= 0 && k < nres;
-    const u32 q0 = ok ? __ldg(res0 + k) : 0u, q1 = ok ? __ldg(res1 + k) : 0u,
-              q2 = ok ? __ldg(res2 + k) : 0u;
-    u32 x0;
-    crt3(q0, q1, q2, x0, P1, P2);
-    if (!ok) P1 = P2 = 0u;
-  }
-#pragma unroll
-  for (int i = 0; i < NR; ++i) crt3(V0[i], V1[i], V2[i], V0[i], V1[i], V2[i]);
-  if (!in_res) {
-#pragma unroll
-    for (int i = 0; i < NR; ++i)
-      if (wb + i * 32 + lane >= nres) V0[i] = V1[i] = V2[i] = 0u;
-  }
-  // column sums S_k = V0[k] + V1[k-1] + V2[k-2] + d[k]
   u64 S[NR];
-#pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    const u32 p1row = i ? V1[i - 1] : P1, p2row = i ? V2[i - 1] : P2;
-    const u32 a1 = __shfl_up_sync(0xFFFFFFFFu, V1[i], 1);
-    const u32 b1 = __shfl_sync(0xFFFFFFFFu, p1row, 31);
-    const u32 a2 = __shfl_up_sync(0xFFFFFFFFu, V2[i], 2);
-    const u32 b2 = __shfl_sync(0xFFFFFFFFu, p2row, 30 + (lane & 1));
-    S[i] = (u64)V0[i] + (lane ? a1 : b1) + (lane >= 2 ? a2 : b2) + DV[i];
+  u64 s_next = 0;
+  if constexpr (CW == 1) {
+    sums_cw1(res, L, job.nRes, wb, last, S, s_next);
+  } else {
+    sums_cw2<LOOKBACK>(res, L, job.nRes, wb, tile, sm, S, s_next);
   }
-  // warp carry function (carry-in 0)
+#pragma unroll
+  for (int i = 0; i < NR; ++i) S[i] += DV[i];
+  // resolve the warp's words with carry-in 0 and its carry function
+  // c -> q + (c >= t): the extra carry needs word 0 + c to overflow and every
+  // other word to be all-ones
   CarryFn f;
+  u32 T[NR];
+  unsigned ones[NR];
   {
     u32 c = 0;
     bool allones = true;
-    u32 first = 0;
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
-      unsigned ones;
-      const u32 t = carry_row(S[i], c, ones);
-      if (i == 0) {
-        first = __shfl_sync(0xFFFFFFFFu, t, 0);
-        ones |= 1u;
-      }
-      allones &= (ones == 0xFFFFFFFFu);
+      T[i] = carry_row(S[i], c, ones[i]);
+      allones &= ((i == 0 ? (ones[i] | 1u) : ones[i]) == 0xFFFFFFFFu);
     }
+    const u32 first = __shfl_sync(0xFFFFFFFFu, T[0], 0);
     f.id = false;
     f.q = c;
     f.t = (allones && first != 0u) ? (0u - first) : kInf;
@@ -408,17 +570,29 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   __syncthreads();
   const u32 tile_cin = sm.cin;
 
-  // final words with the real carry-in
-  u32 c = cf_apply(wpre, tile_cin);
-  u32 T[NR];
+  // add the real carry-in at word 0 and ripple it through all-ones words
+  // (almost always it stops in word 0)
+  const u32 cin_w = cf_apply(wpre, tile_cin);
+  const u32 c = cf_apply(f, cin_w);  // carry out of the warp
+  {
+    u32 cr = cin_w;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      if (cr == 0u) break;
+      const u32 t0 = __shfl_sync(0xFFFFFFFFu, T[i], 0);
+      const bool ov = t0 + cr < cr;
+      if (lane == 0) T[i] = t0 + cr;
+      if (!ov) break;
+      const unsigned stop = ~ones[i] & ~1u;  // lanes >= 1 that absorb the carry
+      const int k = stop ? __ffs(stop) - 1 : 32;
+      if (lane >= 1 && lane < k) T[i] = 0u;
+      if (lane == k) T[i] += 1u;
+      cr = k == 32 ? 1u : 0u;
+    }
+  }
   const long long nT = job.nT;
   const long long rbits = job.n_mod_bits - 32ll * (nT - 1);
   const u32 tmask = rbits >= 32 ? 0xFFFFFFFFu : ((1u << rbits) - 1u);
-#pragma unroll
-  for (int i = 0; i < NR; ++i) {
-    unsigned ones;
-    T[i] = carry_row(S[i], c, ones);
-  }
   if (wb + NR * 32 >= nT) {  // the warp reaches the top word: clear bits >= n_mod_bits
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
@@ -430,15 +604,10 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   // the next tile's first word = S_next + carry
   if (lane == 0) sm.first[warp] = T[0];
   u32 nextw = 0;
-  if (warp == kCarryWarps - 1) {
+  if (last) {
     const long long k = wb + NR * 32;  // first word of the next tile
-    u32 n0 = 0, n1, n2;
-    if (lane == 0) crt_at(res0, res1, res2, k, nres, n0, n1, n2);
-    n0 = __shfl_sync(0xFFFFFFFFu, n0, 0);
-    const u32 v1 = __shfl_sync(0xFFFFFFFFu, V1[NR - 1], 31);
-    const u32 v2 = __shfl_sync(0xFFFFFFFFu, V2[NR - 1], 30);
-    const u32 dv = dw ? fetch_word(dw, k, job.kD, job.maskD) : 0u;
-    const u64 sn = (u64)n0 + v1 + v2 + dv + c;
+    const u32 dv = fetch_word(dw, k, kd, job.maskD);
+    const u64 sn = s_next + dv + c;
     nextw = (u32)sn;
     nextw = k >= nT ? 0u : (k == nT - 1 ? (nextw & tmask) : nextw);
   }
@@ -483,20 +652,22 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
 }
 
 // Decoupled look-back across tiles: one CTA per tile (few, huge blocks).
+template <int CW>
 __global__ void __launch_bounds__(kCarryThreads) k_carry_lb(ConvJob job) {
   __shared__ CarrySmem sm;
   const int b = blockIdx.y;
   if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
   __syncthreads();
-  carry_tile<true>(job, sm, b, (int)sm.tile, 0u);
+  carry_tile<true, CW>(job, sm, b, (int)sm.tile, 0u);
 }
 
 // One CTA per block walking its tiles in order (many blocks): no inter-CTA waits.
+template <int CW>
 __global__ void __launch_bounds__(kCarryThreads) k_carry_seq(ConvJob job) {
   __shared__ CarrySmem sm;
   const int b = blockIdx.y;
   u32 c = 0;
-  for (int tile = 0; tile < job.tiles; ++tile) c = carry_tile<false>(job, sm, b, tile, c);
+  for (int tile = 0; tile < job.tiles; ++tile) c = carry_tile<false, CW>(job, sm, b, tile, c);
 }
 
 
@@ -675,7 +846,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   if (job.m == 1 && job.lgR == 0) {
     const size_t sm = (size_t)sm_len(job.lgC) * 2 * 4;
     prof::Scope ps_("k_row_single", st);
-    row_kernel(job.lgC, true)<<<dim3(1, kNumPrimes, job.batch), threads, sm, st>>>(job, tab, 0);
+    row_kernel(job.lgC, true)<<<dim3(1, job.batch, job.np), threads, sm, st>>>(job, tab, 0);
     return;
   }
   const long long R = (long long)job.m << job.lgR;
@@ -697,7 +868,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   }
   {
     prof::Scope ps_("k_col_fwd", st);
-    cf<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch * 2), threads, smc, st>>>(job, tab, lct);
+    cf<<<dim3(1u << (job.lgC - lct), job.np, job.batch * 2), threads, smc, st>>>(job, tab, lct);
   }
   int lnr = 13 - job.lgC;  // 8K words of rows (A+X: 16K words) per CTA
   if (lnr < 0) lnr = 0;
@@ -705,12 +876,12 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    row_kernel(job.lgC, false)<<<dim3((unsigned)(R >> lnr), kNumPrimes, job.batch), threads, smr,
+    row_kernel(job.lgC, false)<<<dim3((unsigned)(R >> lnr), job.batch, job.np), threads, smr,
                                  st>>>(job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    ci<<<dim3(1u << (job.lgC - lct), kNumPrimes, job.batch), ct_threads, smc, st>>>(job, tab, lct);
+    ci<<<dim3(1u << (job.lgC - lct), job.batch, job.np), ct_threads, smc, st>>>(job, tab, lct);
   }
 }
 
@@ -722,10 +893,18 @@ bool conv_supported(int m, int lgR, int lgC) {
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
   prof::Scope ps_("k_carry", st);
-  if (job.batch >= 2 * 148 || job.tiles == 1) {
-    k_carry_seq<<<dim3(1, job.batch), kCarryThreads, 0, st>>>(job);
+  static const int force = [] {  // development override: PAB_CARRY_MODE=seq|lb
+    const char* e = getenv("PAB_CARRY_MODE");
+    return e ? (e[0] == 's' ? 1 : 2) : 0;
+  }();
+  const bool seq = job.tiles == 1 || (force ? force == 1 : job.batch >= 2 * 148);
+  const dim3 grid(seq ? 1 : job.tiles, job.batch);
+  if (job.cw == 2) {
+    if (seq) k_carry_seq<2><<<grid, kCarryThreads, 0, st>>>(job);
+    else k_carry_lb<2><<<grid, kCarryThreads, 0, st>>>(job);
   } else {
-    k_carry_lb<<<dim3(job.tiles, job.batch), kCarryThreads, 0, st>>>(job);
+    if (seq) k_carry_seq<1><<<grid, kCarryThreads, 0, st>>>(job);
+    else k_carry_lb<1><<<grid, kCarryThreads, 0, st>>>(job);
   }
 }
 

@@ -6,34 +6,29 @@
 
 namespace pab {
 
-// Device twiddle tables for one plan (one transform length L = 2^lg).
-// All arrays are [prime][dir][4096] with dir 0 = forward (w), 1 = inverse (w^-1).
+// Device twiddle tables for one plan (one transform length L = m * 2^lg).
+// Arrays are [prime][dir][...] with dir 0 = forward (w), 1 = inverse (w^-1);
+// primes whose 2-adicity is below lg have zero entries (unused: cw = 1 jobs).
 struct PlanTables {
   const uint2* stw;    // stage twiddles tw[h+e] = w_{2h}^e (Shoup pairs), h <= 2048
-  const u32* tlo_m;    // [3][2][4096] Montgomery form of w_L^e, e < 4096
-  const uint2* thi;    // [3][2][thi_stride] Shoup pairs of w_L^(4096 j)
-  const uint2* g;      // [3][2][R] Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row twiddle step)
-  const uint2* trad;   // [3][2][R] Shoup pairs of w_R^e, e < R (radix-m column stage), or null
+  const u32* tlo_m;    // [5][2][4096] Montgomery form of w_L^e, e < 4096
+  const uint2* thi;    // [5][2][thi_stride] Shoup pairs of w_L^(4096 j)
+  const uint2* g;      // [5][2][R] Shoup pairs of w_L^(k1 * 2^slo0(lgC)), k1 < R (row twiddle step)
+  const uint2* trad;   // [5][2][R] Shoup pairs of w_R^e, e < R (radix-m column stage), or null
   int tstride;         // R: stride of g and trad
   int thi_stride;      // stride of thi (>= L / 4096)
-  const uint2* tw4;    // [3][2][L] full four-step twiddles w_L^(+-c*brev(q)) at [q*C + c],
+  const uint2* tw4;    // [5][2][L] full four-step twiddles w_L^(+-c*brev(q)) at [q*C + c],
                        // Shoup pairs; only for small L (L2-resident), else null
-  u32 scale[3];        // L^-1 * 2^32 mod p: undoes the length and the Montgomery factor
-  u32 scale_sh[3];     // of the pointwise product (Shoup companions)
-};
-
-struct CrtConst {
-  u32 p0, p1, p2;
-  u32 inv01, inv01_sh;     // p0^-1 mod p1
-  u32 p0m2, p0m2_sh;       // p0 mod p2
-  u32 inv012, inv012_sh;   // (p0 p1)^-1 mod p2
-  u64 p0p1;
+  u32 scale[kNumPrimes];     // L^-1 * 2^32 mod p: undoes the length and the Montgomery
+  u32 scale_sh[kNumPrimes];  // factor of the pointwise product (Shoup companions)
 };
 
 // One convolution-product job over a batch of independent blocks:
 //   T = (A * X + D) mod 2^n_mod_bits (as 32-bit words), out = T >> shift.
 struct ConvJob {
   int batch;
+  int cw;                      // words per coefficient: 2 (five primes) or 1 (three primes)
+  int np;                      // primes (grid.y of the conv kernels): 5 if cw == 2 else 3
   int m;                       // radix of the column length: L = m * 2^lg
   int lg, lgR, lgC;            // R = m * 2^lgR rows (columns of length R), C = 2^lgC
   long long L;                 // transform length (R = 1: single-CTA path)
@@ -41,12 +36,12 @@ struct ConvJob {
   const u32* srcA;
   const u32* srcX;
   const u32* srcD;             // may be null (no addend)
-  long long src_stride;        // in words
+  long long src_stride;        // in words (even when cw == 2: 8-byte aligned coefficients)
   long long kA, kX, kD;        // valid words per block
   u32 maskA, maskX, maskD;     // applied to the last valid word (bits >= n)
-  u32* buf;                    // [batch][2][3][L] transform buffers (slot A reused for residues)
+  u32* buf;                    // [batch][2][np][L] transform buffers (slot A reused for residues)
   long long nT;                // T words computed
-  long long nRes;              // residues stored (min(nT, L))
+  long long nRes;              // residues stored per prime (coefficients: <= L)
   long long n_mod_bits;        // T is reduced mod 2^n_mod_bits
   long long shift;             // output = T >> shift
   long long mw;                // output words per block
@@ -66,7 +61,6 @@ constexpr int kCarryTile = 32 * kCarryWarps * kCarryRows;  // words per tile
 
 constexpr int kTinyBits = 2048;  // single-warp schoolbook path (n <= kTinyBits)
 
-void upload_constants(const CrtConst& crt);
 void launch_tiny(const uint8_t* x, const uint8_t* c, const uint8_t* d, long long stride, int n_bits,
                  int r_bits, int msf, int batch, uint8_t* out, long long out_stride,
                  cudaStream_t st);

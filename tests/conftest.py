@@ -28,3 +28,16 @@ def config_golden():
         pytest.skip("configs.json golden digests not generated")
     with open(path) as f:
         return json.load(f)
+
+
+@pytest.fixture(params=[2, 1], ids=["coef64x5", "coef32x3"])
+def coef_words(request):
+    """Run a GPU test in both convolution modes: 64-bit coefficients over five
+    primes (the default up to 121,295,104 bits) and 32-bit over three (beyond)."""
+    from paper_1910_04429_b200 import _native
+
+    _native.force_coef_words(request.param)
+    try:
+        yield request.param
+    finally:
+        _native.force_coef_words(0)

@@ -42,17 +42,33 @@ def test_host_only_queries():
     lib = _native.load()
     assert lib.pab_version() == 101
     assert _native.max_bits() == 32 * ((5 * 2**22 + 1) // 2)
-    # L = m * 2^lg: pow2 at 1e6, radix-5 at 1e7 (655360), radix-3 at 1e8 (6291456)
-    assert _native.plan_info(10**6) == (1, 16, 8, 8)
-    assert _native.plan_info(10**7) == (5, 17, 7, 10)
-    assert _native.plan_info(10**8) == (3, 21, 9, 12)
+    # 64-bit coefficients over five primes (K' = ceil(n/64)), L = m * 2^lg >= 2K' - 1:
+    # pow2 at 1e6 (32768), radix-5 at 1e7 (327680), radix-3 at 1e8 (3145728)
+    assert _native.plan_info(10**6) == (1, 15, 7, 8)
+    assert _native.plan_info(10**7) == (5, 16, 6, 10)
+    assert _native.plan_info(10**8) == (3, 20, 9, 11)
     assert _native.plan_info(4) == (1, 6, 0, 6)
+    # the five-prime CRT bound K' * (2^64-1)^2 < P ends at K' = 1,895,236; beyond it
+    # 32-bit coefficients over three primes (2-adicity 22) reach 5 * 2^22
+    for n in (1, 10**6, 10**8, 121_295_104):
+        assert _native.plan_width(n) == (64, 5)
+    for n in (121_295_105, _native.max_bits()):
+        assert _native.plan_width(n) == (32, 3)
     for n in (1, 33, 2047, 2049, 65537, 131_072 * 32, 3 * 10**6, 5 * 10**7, 1 << 27,
               _native.max_bits()):
         m, lg, lr, lc = _native.plan_info(n)
-        K = (n + 31) // 32
+        bits, primes = _native.plan_width(n)
+        K = (n + bits - 1) // bits
         assert (m << lg) >= 2 * K - 1 and m in (1, 3, 5)
-    assert lib.pab_hash_workspace_bytes(10**6, 1) > 6 * 4 * (1 << 16)
+        assert lg <= (20 if primes == 5 else 22)
+    _native.force_coef_words(1)
+    try:
+        assert _native.plan_width(10**6) == (32, 3)
+        assert _native.plan_info(10**6) == (1, 16, 8, 8)
+    finally:
+        _native.force_coef_words(0)
+    assert _native.plan_width(10**6) == (64, 5)
+    assert lib.pab_hash_workspace_bytes(10**6, 1) > 10 * 4 * (1 << 15)
     assert lib.pab_hash_workspace_bytes(0, 1) == 0
     rc = lib.pab_plan_info(0, None, None, None, None)
     assert rc == _native.PAB_EINVAL

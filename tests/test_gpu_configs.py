@@ -113,7 +113,7 @@ def test_prefix_property_and_offset_linearity():
 
 
 @pytest.mark.parametrize("batch", [1, 300])
-def test_unaligned_shift_across_tiles(batch):
+def test_unaligned_shift_across_tiles(batch, coef_words):
     # (n - r) % 32 != 0 with outputs spanning many carry tiles, in both the
     # look-back (few blocks) and the sequential (many blocks) carry modes
     n = 300_007 if batch > 1 else 3_000_013
@@ -147,11 +147,11 @@ def test_max_size_and_range_errors(n):
             _native.hash_host(x + b"\0", bytes(c) + b"\0", d + b"\0", n + 1, 5)
 
 
-def _plan_sweep_sizes():
-    """One block size per distinct (radix, lg_rows, lg_cols) plan up to 2^27 bits."""
+def _plan_sweep_sizes(limit=1 << 27):
+    """One block size per distinct (radix, lg_rows, lg_cols) plan up to `limit` bits."""
     seen, sizes = set(), []
     n = 2000
-    while n < (1 << 27):
+    while n < limit:
         key = _native.plan_info(n)
         if key not in seen:
             seen.add(key)
@@ -160,8 +160,9 @@ def _plan_sweep_sizes():
     return sizes
 
 
-def test_every_transform_plan_matches_oracle():
-    sizes = _plan_sweep_sizes()
+def test_every_transform_plan_matches_oracle(coef_words):
+    # forced 64-bit coefficients end at the five-prime CRT bound
+    sizes = _plan_sweep_sizes(1 << 27 if coef_words == 1 else 121_295_104)
     radices = {_native.plan_info(n)[0] for n in sizes}
     assert radices == {1, 3, 5}, radices
     rng = np.random.default_rng(77)
@@ -200,7 +201,7 @@ def test_ten_million_bit_product():
     assert pab.mul(a, b).value == oracle.mul(a, b)
 
 
-def test_unbalanced_and_trivial_products():
+def test_unbalanced_and_trivial_products(coef_words):
     rng = random.Random(6)
     for _ in range(30):
         a = rng.getrandbits(rng.randrange(1, 400_000))

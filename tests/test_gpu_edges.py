@@ -26,7 +26,7 @@ def _rand_blocks(rng, n, B, odd=True):
 
 @pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 2047, 2048, 2049, 4096, 65_504, 65_536,
                                65_537, 65_600])
-def test_size_class_boundaries(n):
+def test_size_class_boundaries(n, coef_words):
     # tiny (<= 2048 bits, host path), single-CTA (L <= 4096), four-step
     rng = np.random.default_rng(n)
     arr = _rand_blocks(rng, n, 3)

@@ -29,7 +29,24 @@ def test_small_golden_hash_cases(small_golden):
     assert not bad, f"{len(bad)} mismatches: {bad[:10]}"
 
 
-def test_small_golden_products(small_golden):
+def test_small_golden_device_path_both_modes(small_golden, coef_words):
+    # every small golden case through the batched device path (no tiny kernel)
+    import torch
+
+    from paper_1910_04429_b200.batch import HashEngine
+
+    bad = []
+    for case in small_golden["hash"]:
+        x, c, d, order = _case_bytes(case)
+        dev = [torch.frombuffer(bytearray(v), dtype=torch.uint8).view(1, -1).cuda()
+               for v in (x, c, d)]
+        out = HashEngine(case["n"], case["r"], order=order, max_batch=1).hash_device(*dev)
+        if out.cpu().numpy().tobytes() != bytes.fromhex(case["y"]):
+            bad.append((case["tag"], case["n"], case["r"], case["order"]))
+    assert not bad, f"{len(bad)} mismatches: {bad[:10]}"
+
+
+def test_small_golden_products(small_golden, coef_words):
     for case in small_golden["mul"]:
         a, b, p = int(case["a"], 16), int(case["b"], 16), int(case["p"], 16)
         assert pab.mul(a, b).value == p, (a.bit_length(), b.bit_length())
