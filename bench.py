@@ -95,7 +95,9 @@ def plan_geometry(n: int) -> dict:
     from paper_1910_04429_b200 import _native
 
     m, lg, lr, lc = _native.plan_info(n)
-    return {"m": m, "lg": lg, "lgR": lr, "lgC": lc, "L": m << lg, "K": (n + 31) // 32}
+    cbits, primes = _native.plan_width(n)
+    return {"m": m, "lg": lg, "lgR": lr, "lgC": lc, "L": m << lg, "K": (n + 31) // 32,
+            "Kc": (n + cbits - 1) // cbits, "cw": cbits // 32, "P": primes}
 
 
 def kernel_model(n: int, r: int, blocks: int) -> dict:
@@ -103,28 +105,34 @@ def kernel_model(n: int, r: int, blocks: int) -> dict:
 
     Bytes count what the kernel must move at least once; int ops count the
     canonical 7 ops per radix-2 butterfly (Harvey/Shoup lazy butterfly, 3 on
-    the FMA pipe + 4 on the ALU pipe), 6 per Montgomery product and 8 per
-    four-step twiddle application.
+    the FMA pipe + 4 on the ALU pipe), 6 per Montgomery product, 8 per
+    four-step twiddle application, 3 (9 for a 64-bit coefficient) per input
+    reduction and a Garner CRT of 35 (3 primes) / 85 (5 primes) ops per
+    coefficient plus 25 per output word for the carry.  K = words, Kc =
+    coefficients (K / cw), P = NTT primes of the plan's mode.
     """
     g = plan_geometry(n)
-    L, K, lgR, lgC, mr = g["L"], g["K"], g["lgR"], g["lgC"], g["m"]
+    L, K, Kc, lgR, lgC, mr = g["L"], g["K"], g["Kc"], g["lgR"], g["lgC"], g["m"]
     nb, rb, mw = (n + 7) // 8, (r + 7) // 8, (r + 31) // 32
-    P = 3
+    P = g["P"]
+    red_in = L * 3 + (Kc * 6 if g["cw"] == 2 else 0)
+    crt = {3: 35, 5: 85}[P]
     rad = {1: 0, 3: 25, 5: 56}[mr]  # ops per radix-m group (incl. its twiddles)
     bf = lambda lg: (L // 2) * lg  # butterflies of one length-L transform restricted to lg stages
     m = {}
     m["k_pack"] = dict(bytes=blocks * 3 * (nb + 4 * K), ops=0)
     m["k_unpack"] = dict(bytes=blocks * (4 * mw + rb), ops=0)
-    m["k_carry"] = dict(bytes=blocks * (P * 4 * K + 4 * K + 4 * mw), ops=blocks * K * 60)
+    m["k_carry"] = dict(bytes=blocks * (P * 4 * Kc + 4 * K + 4 * mw),
+                        ops=blocks * (Kc * crt + K * 25))
     if lgR == 0:
-        m["k_row_single"] = dict(bytes=blocks * (2 * 4 * K + P * 4 * K),
-                                 ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 2 * L * 3))
+        m["k_row_single"] = dict(bytes=blocks * (2 * 4 * K + P * 4 * Kc),
+                                 ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 2 * red_in))
     else:
         m["k_col_fwd"] = dict(bytes=blocks * 2 * (4 * K + P * 4 * L),
-                              ops=blocks * 2 * P * (bf(lgR) * 7 + L * 3 + (L // mr) * rad))
+                              ops=blocks * 2 * P * (bf(lgR) * 7 + red_in + (L // mr) * rad))
         m["k_row"] = dict(bytes=blocks * P * 3 * 4 * L,
                           ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 3 * L * 8))
-        m["k_col_inv"] = dict(bytes=blocks * P * (4 * L + 4 * K),
+        m["k_col_inv"] = dict(bytes=blocks * P * (4 * L + 4 * Kc),
                               ops=blocks * P * (bf(lgR) * 7 + L * 4 + (L // mr) * rad))
     return m
 

@@ -81,6 +81,33 @@ __device__ __forceinline__ u32 coef_at(const OpView& o, int gi) {
   return coef_red<P>(lo, hi, o.cw);
 }
 
+// Forward column grid (1-D): chunks of fwd_chunk blocks, then prime, then
+// block, operand, column tile.  All primes of a chunk read the same operand
+// words, which stay L2-resident across the chunk's five prime sweeps, while
+// the CTAs resident together run one prime's code.
+struct FwdIdx {
+  int prime, b, op, tile;
+};
+__device__ __forceinline__ FwdIdx fwd_idx(const ConvJob& job, int lct) {
+  const unsigned tc = 1u << (job.lgC - lct);
+  const unsigned per_block = 2u * tc;  // CTAs of one (block, prime)
+  const unsigned span = per_block * (unsigned)job.np * (unsigned)job.fwd_chunk;
+  const unsigned id = blockIdx.x;
+  const unsigned c = id / span;
+  const unsigned local = id - c * span;
+  const int b0 = (int)c * job.fwd_chunk;
+  const int nb = min(job.fwd_chunk, job.batch - b0);
+  const unsigned per_prime = per_block * (unsigned)nb;
+  FwdIdx r;
+  r.prime = (int)(local / per_prime);
+  const unsigned rem = local - (unsigned)r.prime * per_prime;
+  r.b = b0 + (int)(rem / per_block);
+  const unsigned w = rem - (rem / per_block) * per_block;
+  r.op = (int)(w / tc);
+  r.tile = (int)(w - (unsigned)r.op * tc);
+  return r;
+}
+
 // conv kernels run one prime per grid index IDX (job.np of them).  Kernels
 // without cross-prime data reuse (row, inverse column) put the prime in the
 // slowest grid dimension so CTAs resident together run the same prime's
@@ -340,15 +367,15 @@ __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int ln
 // broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
 // scaled residues.
 template <int P, int LGR, int LGC>
-__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
+__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
+                                             int b, int op, int tile) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
   const int CT = 1 << lct;
-  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
   constexpr int lgC = LGC;
   const long long L = job.L;
-  const int c0 = blockIdx.x << lct;
+  const int c0 = tile << lct;
   const OpView ov = op_view(job, op, b);
   u32* dst = job.buf + (((long long)b * 2 + op) * job.np + P) * L;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
@@ -542,15 +569,15 @@ __device__ __forceinline__ void colm_pass(u32* smem, int lct, const uint2* __res
 }
 
 template <int P, int M, int LGR2, int LGC>
-__device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTables& tab, int lct) {
+__device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
+                                             int b, int op, int tile) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR2);
   constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
   const int CT = 1 << lct;
-  const int b = blockIdx.z >> 1, op = blockIdx.z & 1;
   constexpr int lgC = LGC;
   const long long L = job.L;
-  const int c0 = blockIdx.x << lct;
+  const int c0 = tile << lct;
   const OpView ov = op_view(job, op, b);
   u32* dst = job.buf + (((long long)b * 2 + op) * job.np + P) * L;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
@@ -724,9 +751,10 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
 }
 
 template <int M, int LGR2, int LGC>
-__global__ void __launch_bounds__(256) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
-#define PAB_B(P_) colm_fwd_body<P_, M, LGR2, LGC>(job, tab, lct);
-  PAB_PRIME_SWITCH(PAB_B, blockIdx.y)
+__global__ void __maxnreg__(48) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
+  const FwdIdx ix = fwd_idx(job, lct);
+#define PAB_B(P_) colm_fwd_body<P_, M, LGR2, LGC>(job, tab, lct, ix.b, ix.op, ix.tile);
+  PAB_PRIME_SWITCH(PAB_B, ix.prime)
 #undef PAB_B
 }
 template <int M, int LGR2, int LGC>
@@ -738,8 +766,9 @@ __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, i
 
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
-#define PAB_B(P_) col_fwd_body<P_, LGR, LGC>(job, tab, lct);
-  PAB_PRIME_SWITCH(PAB_B, blockIdx.y)
+  const FwdIdx ix = fwd_idx(job, lct);
+#define PAB_B(P_) col_fwd_body<P_, LGR, LGC>(job, tab, lct, ix.b, ix.op, ix.tile);
+  PAB_PRIME_SWITCH(PAB_B, ix.prime)
 #undef PAB_B
 }
 template <int LGR, int LGC>

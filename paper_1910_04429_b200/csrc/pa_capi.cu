@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <atomic>
@@ -102,18 +103,27 @@ bool choose_geo(u64 need, int maxlg, Geo* out) {
     g.m = m;
     g.lg = lg;
     g.L = (u64)m << lg;
+    static const int force_lgc = [] {  // development override of the four-step split
+      const char* e = getenv("PAB_LGC");
+      return e ? atoi(e) : 0;
+    }();
     if (m == 1) {
       if (lg <= kTwLg) {
         g.lgR = 0;
         g.lgC = lg;
       } else {
-        g.lgR = lg / 2;
-        g.lgC = lg - lg / 2;
+        g.lgC = force_lgc ? force_lgc : lg - lg / 2;
+        g.lgR = lg - g.lgC;
       }
     } else {
       if (g.L <= (u64)kTwN) continue;  // small lengths: single-CTA pow2 path
       const double lgm = m == 3 ? 1.585 : 2.322;
       int lgC = (int)std::ceil((lg + lgm) / 2.0);  // rows >= columns: smaller column panels
+      // measured exceptions (profiles/README.md, split sweep): the row kernel is
+      // most efficient at lgC = 9, and 3 * 2^20 prefers the shorter columns
+      if (m == 5 && lg == 16) lgC = 9;
+      if (m == 3 && lg == 20) lgC = 12;
+      if (force_lgc) lgC = force_lgc;
       if (lgC > kTwLg) lgC = kTwLg;
       if (lgC < 6) lgC = 6;
       g.lgC = lgC;

@@ -829,6 +829,7 @@ static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
 static int col_lct(int lgR, int lgC) {
   int lct = 14 - lgR;  // ~16K words per CTA
   if (lct > 5) lct = 5;
+  if (lct < 13 - lgR) lct = 13 - lgR;  // the radix-32 pass has >= 256 tasks (one per thread)
   if (lct < 3) lct = 3;
   if (lct > lgC) lct = lgC;
   return lct;
@@ -856,19 +857,30 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
                              : colm_kernel(job.m, job.lgR, job.lgC, false);
   ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true)
                              : colm_kernel(job.m, job.lgR, job.lgC, true);
-  // mixed-radix inverse: one thread per task of its first pow2 pass (M * CT * 2^(lgR-5)
-  // tasks; 256 threads would leave e.g. 384 tasks at 75% utilisation).  The forward
-  // kernel keeps 256 threads: its register count would halve the resident CTAs.
-  int ct_threads = threads;
+  // mixed radix: one thread per task of the radix-32 pow2 pass (M * CT * 2^(lgR-5)
+  // tasks; 256 threads would leave e.g. 320 tasks at 62% utilisation).  The
+  // forward kernel does so only when its first pass has at least as many tasks
+  // (else those threads idle there and cost resident CTAs).
+  int ct_threads = threads, cf_threads = threads;
   if (job.m > 1) {
-    const int lastrs = pass_plan(job.lgR).rs[pass_plan(job.lgR).n - 1];
-    ct_threads = (job.m << lct) << (job.lgR - lastrs);
+    const PassPlan pp = pass_plan(job.lgR);
+    const int tasks_last = (job.m << lct) << (job.lgR - pp.rs[pp.n - 1]);
+    ct_threads = tasks_last;
     while (ct_threads > 512) ct_threads >>= 1;
     if (ct_threads < 128) ct_threads = 128;
+    const bool fuse = pp.n >= 2 && (job.m << pp.rs[0]) <= 32;  // conv_kernels.cuh: colm_fwd_body
+    const int tasks_first = fuse ? (1 << (lct + pp.slo[0])) : (1 << (lct + job.lgR));
+    if (tasks_last <= 512 && tasks_first >= tasks_last) cf_threads = ct_threads;
   }
   {
     prof::Scope ps_("k_col_fwd", st);
-    cf<<<dim3(1u << (job.lgC - lct), job.np, job.batch * 2), threads, smc, st>>>(job, tab, lct);
+    // ~32 MiB of operand words per chunk (L2-resident across the prime sweeps)
+    ConvJob jf = job;
+    const long long kmax = job.kA > job.kX ? job.kA : job.kX;
+    long long chunk = (32ll << 20) / (8 * kmax);
+    jf.fwd_chunk = (int)(chunk < 1 ? 1 : (chunk > job.batch ? job.batch : chunk));
+    const unsigned ctas = (1u << (job.lgC - lct)) * 2u * (unsigned)job.np * (unsigned)job.batch;
+    cf<<<ctas, cf_threads, smc, st>>>(jf, tab, lct);
   }
   int lnr = 13 - job.lgC;  // 8K words of rows (A+X: 16K words) per CTA
   if (lnr < 0) lnr = 0;

@@ -52,6 +52,7 @@ struct ConvJob {
   unsigned long long* tile_state;  // [batch][tiles] look-back states (zeroed)
   u32* tile_ctr;               // [batch] tile tickets (zeroed)
   int tiles;                   // carry tiles per block
+  int fwd_chunk;               // forward column pass: blocks per L2-resident chunk (grid order)
 };
 
 constexpr int kCarryWarps = 8;                           // warps per carry CTA

@@ -11,6 +11,10 @@ if len(sys.argv) > 1:
 modes = [int(v) for v in os.environ.get("QP_CW", "0").split(",")]
 for n, r, B, cw in [(n, r, B, cw) for (n, r, B) in cases for cw in modes]:
     _native.force_coef_words(cw)
+    try:
+        _native.plan_info(n)
+    except ValueError:
+        continue
     nb = (n + 7) // 8
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randint(0, 256, (B, nb), dtype=torch.uint8, device="cuda", generator=g)
