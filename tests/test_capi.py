@@ -45,8 +45,8 @@ def test_host_only_queries():
     # 64-bit coefficients over five primes (K' = ceil(n/64)), L = m * 2^lg >= 2K' - 1:
     # pow2 at 1e6 (32768), radix-5 at 1e7 (327680), radix-3 at 1e8 (3145728)
     assert _native.plan_info(10**6) == (1, 15, 7, 8)
-    assert _native.plan_info(10**7) == (5, 16, 6, 10)
-    assert _native.plan_info(10**8) == (3, 20, 9, 11)
+    assert _native.plan_info(10**7) == (5, 16, 7, 9)
+    assert _native.plan_info(10**8) == (3, 20, 8, 12)
     assert _native.plan_info(4) == (1, 6, 0, 6)
     # the five-prime CRT bound K' * (2^64-1)^2 < P ends at K' = 1,895,236; beyond it
     # 32-bit coefficients over three primes (2-adicity 22) reach 5 * 2^22
