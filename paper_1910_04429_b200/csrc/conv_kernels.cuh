@@ -241,9 +241,8 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
     constexpr int LGG = LGC - RSL;
     for (int task = threadIdx.x; task < (NR << LGG); task += blockDim.x) {
       const int row = task >> LGG, g = task & ((1 << LGG) - 1);
-      u32 a[1][1 << RSL], x[1][1 << RSL];
-      int base = 0;
       if constexpr (PP.n == 1) {  // whole transform in registers, straight from global
+        u32 a[1][1 << RSL], x[1][1 << RSL];
         const int q = q0 + row;
         if constexpr (SMALL) {
 #pragma unroll
@@ -262,20 +261,11 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             m = shoup(m, gam, PK<P>::p);
           }
         }
-      } else {
-        base = row * T + sm_idx(g << RSL);
+        dif_ct<P, RSL, 1>(a);
+        dif_ct<P, RSL, 1>(x);
 #pragma unroll
-        for (int k = 0; k < (1 << RSL); ++k) a[0][k] = sA[base + k];
-#pragma unroll
-        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = sX[base + k];
-      }
-      dif_ct<P, RSL, 1>(a);
-      dif_ct<P, RSL, 1>(x);
-#pragma unroll
-      for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
-      dit_ct<P, RSL>(x[0]);
-      if constexpr (PP.n == 1) {
-        const int q = q0 + row;
+        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
+        dit_ct<P, RSL>(x[0]);
         if constexpr (SMALL) {
 #pragma unroll
           for (int k = 0; k < (1 << RSL); ++k)
@@ -291,9 +281,40 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             m = shoup(m, gam, PK<P>::p);
           }
         }
-      } else {
+      } else if constexpr (LGC > 8) {
+        const int base = row * T + sm_idx(g << RSL);
+        u32 a[1][1 << RSL], x[1][1 << RSL];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) a[0][k] = sA[base + k];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = sX[base + k];
+        dif_ct<P, RSL, 1>(a);
+        dif_ct<P, RSL, 1>(x);
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) x[0][k] = mont<P>(a[0][k], x[0][k]);
+        dit_ct<P, RSL>(x[0]);
 #pragma unroll
         for (int k = 0; k < (1 << RSL); ++k) sX[base + k] = x[0][k];
+      } else {
+        // lgC <= 8 (measured faster): A and X one after the other (32 live
+        // values, not 64; 79 -> 64 registers): A's spectrum goes back to smem
+        // and is re-read per point for the pointwise product.
+        const int base = row * T + sm_idx(g << RSL);
+        u32 v[1][1 << RSL];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) v[0][k] = sA[base + k];
+        dif_ct<P, RSL, 1>(v);
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) sA[base + k] = v[0][k];
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) v[0][k] = sX[base + k];
+        dif_ct<P, RSL, 1>(v);
+        asm volatile("" ::: "memory");  // compiler barrier: re-read A (tasks may be < 32 per warp)
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) v[0][k] = mont<P>(sA[base + k], v[0][k]);
+        dit_ct<P, RSL>(v[0]);
+#pragma unroll
+        for (int k = 0; k < (1 << RSL); ++k) sX[base + k] = v[0][k];
       }
     }
   }

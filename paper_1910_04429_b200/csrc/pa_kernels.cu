@@ -857,20 +857,17 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
                              : colm_kernel(job.m, job.lgR, job.lgC, false);
   ConvKernel ci = job.m == 1 ? col_kernel(job.lgR, job.lgC, true)
                              : colm_kernel(job.m, job.lgR, job.lgC, true);
-  // mixed radix: one thread per task of the radix-32 pow2 pass (M * CT * 2^(lgR-5)
-  // tasks; 256 threads would leave e.g. 320 tasks at 62% utilisation).  The
-  // forward kernel does so only when its first pass has at least as many tasks
-  // (else those threads idle there and cost resident CTAs).
-  int ct_threads = threads, cf_threads = threads;
-  if (job.m > 1) {
-    const PassPlan pp = pass_plan(job.lgR);
-    const int tasks_last = (job.m << lct) << (job.lgR - pp.rs[pp.n - 1]);
-    ct_threads = tasks_last;
-    while (ct_threads > 512) ct_threads >>= 1;
-    if (ct_threads < 128) ct_threads = 128;
-    const bool fuse = pp.n >= 2 && (job.m << pp.rs[0]) <= 32;  // conv_kernels.cuh: colm_fwd_body
-    const int tasks_first = fuse ? (1 << (lct + pp.slo[0])) : (1 << (lct + job.lgR));
-    if (tasks_last <= 512 && tasks_first >= tasks_last) cf_threads = ct_threads;
+  // mixed-radix inverse: 512 threads for radix 3 (its 384-task first pass and
+  // 512-task fused radix pass), 256 otherwise; the forward pass keeps 256
+  // (measured: scripts/quick_perf.py with PAB_CI_THREADS / PAB_CF_THREADS).
+  int ct_threads = job.m == 3 ? 512 : threads;
+  const int cf_threads = threads;
+  {
+    static const int force_ci = [] {  // development override
+      const char* e = getenv("PAB_CI_THREADS");
+      return e ? atoi(e) : 0;
+    }();
+    if (force_ci && job.m > 1) ct_threads = force_ci;
   }
   {
     prof::Scope ps_("k_col_fwd", st);

@@ -4,7 +4,7 @@ TAG=${1:-r1}
 make -s -C oracle
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu_${TAG}.txt
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -3 | tee gpurun_out/pytest_gpu_${TAG}.log
+timeout 900 python -m pytest tests -q -m gpu --timeout 300 2>&1 | tail -3 | tee gpurun_out/pytest_gpu_${TAG}.log
 /tmp/int_peak > gpurun_out/int_peak_${TAG}.json 2>/dev/null || (nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/int_peak scripts/int_peak.cu && /tmp/int_peak > gpurun_out/int_peak_${TAG}.json)
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err
 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
