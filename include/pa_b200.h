@@ -45,7 +45,7 @@ extern "C" {
 int pab_version(void);
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* pab_last_error(void);
-/* Largest block size n (bits) the exact three-prime convolution supports. */
+/* Largest block size n (bits) the exact convolution supports (32-bit coefficients, three primes). */
 uint64_t pab_max_bits(void);
 
 /*

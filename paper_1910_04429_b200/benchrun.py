@@ -29,7 +29,7 @@ from .bignum import BigNat, mul
 from .runpa import RunConfig, resolve_out_bits
 
 BENCH_CSV_COLUMNS = ("block_size", "algorithm", "trials", "elapsed_ms", "throughput_mbps")
-ALGORITHM = "b200-ntt3"  # three-prime NTT convolution on the GPU
+ALGORITHM = "b200-ntt"  # multi-prime NTT convolution on the GPU
 
 
 @dataclass(frozen=True)

@@ -6,7 +6,7 @@ switch modules.  The product ``mul`` (bignum.py:194-231) and
 ``fused_mul_add`` (bignum.py:234-238) run on the B200 through the C ABI
 (``pab_mul_host``); ``alg`` and ``thresholds`` are accepted and ignored
 because every route returns the identical exact product by contract
-(bignum.py:197-201) -- the GPU's three-prime NTT replaces all four.
+(bignum.py:197-201) -- the GPU's multi-prime NTT replaces all four.
 ``mod_pow2`` / ``shift_right`` are single bit-mask / shift operations on the
 host int, exactly as in the reference (bignum.py:161-172); on the hash path
 they are fused into the GPU carry kernel instead.

@@ -1,4 +1,5 @@
-# Round evidence: GPU tests, bench (both arms), launch list + ncu of the bench command.
+# Round evidence: GPU tests, bench (both arms), launch list of the bench command.
+# (The --set full capture is a separate call: scripts/gpu_ncu_full.sh; one ncu per call.)
 set -e
 TAG=${1:-r1}
 make -s -C oracle
@@ -12,7 +13,4 @@ python bench.py --config C5 --steps 20 --no-cpu > gpurun_out/bench_C5_${TAG}.jso
 CMD="python bench.py --steps 3 --warmup 3 --no-extra --no-cpu"
 $CMD > gpurun_out/plain_bench.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-CMD2="python scripts/quick_perf.py 1e6,5e5,1024"
-$CMD2 > gpurun_out/plain_qp.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_row|k_col|k_carry" -s 4 -c 4 -o gpurun_out/prof_${TAG} $CMD2 > gpurun_out/ncu_full.log 2>&1
 echo done
