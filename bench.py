@@ -318,9 +318,33 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
     clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist)
     assert torch.equal(hout, first_out), "e2e keys differ from device-resident keys"
+    # the PCIe bound of that leg: the same pinned H2D + D2H bytes, copies only
+    # (H2D and D2H overlapped on two streams, as hash_host overlaps them)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(2, min(args.steps, 10))
+    torch.cuda.synchronize()
+    c0.record(st)
+    s_in.wait_stream(st)
+    s_out.wait_stream(st)
+    for _ in range(reps):
+        with torch.cuda.stream(s_in):
+            dx.copy_(px, non_blocking=True)
+            dc.copy_(pc, non_blocking=True)
+            dd.copy_(pd, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            hout.copy_(dout, non_blocking=True)
+    st.wait_stream(s_in)
+    st.wait_stream(s_out)
+    c1.record(st)
+    torch.cuda.synchronize()
+    copy_ms = max_over_ranks(c0.elapsed_time(c1) / reps, dist)
     e2e = {"value": round(bits_step / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
            "h2d_bytes_per_step": 3 * per_rank * eng.nbytes,
-           "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(e2e_ms, 4)}
+           "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(e2e_ms, 4),
+           "copy_only_ms_per_step": round(copy_ms, 4),
+           "h2d_gbps": round(3 * per_rank * eng.nbytes / (e2e_ms * 1e-3) / 1e9, 1),
+           "frac_of_copy_bound": round(copy_ms / e2e_ms, 4)}
 
     res = {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
            "out": first_out, "per_rank": per_rank, "n": n, "r": r, "eng": eng,
