@@ -435,7 +435,7 @@ def main():
     if args.config in ("C4", "C5"):
         cfg["cpu_blocks"] = 2
         cfg["ref_blocks"] = 1
-        cfg["chunk"] = 8
+        cfg["chunk"] = 16  # one launch per 16-block step (2.0 GiB workspace; 8-block launches 2% slower)
         cfg["e2e_chunk"] = 2
         if args.config == "C5":
             cfg["seeds"] = tuple(range(16))  # 16 blocks/rank per step (1.6 Gbit)
