@@ -11,8 +11,10 @@ struct ConvKernels {
   ConvKernel row, row_small;
   ConvKernel col_fwd, col_inv;      // column passes with lgC == LG (lg even)
   ConvKernel col_fwd1, col_inv1;    // column passes with lgC == LG + 1 (lg odd)
+  ConvKernel col_fwd_all, col_fwd_all1;  // all-primes forward column pass (lgC == LG, LG + 1)
   // mixed radix M = 3, 5 (index 0, 1) with LGR2 == LG and lgC = LG + 2 + dc (dc = 0..2)
   ConvKernel colm_fwd[2][3], colm_inv[2][3];
+  ConvKernel colm_fwd_all[2][3];
 };
 
 __device__ __forceinline__ int brev(int x, int bits) {
@@ -61,6 +63,24 @@ __device__ __forceinline__ u32 coef_fast(const OpView& o, int gi) {
   }
   return coef_red<P>(__ldg(o.src + gi), 0u, 1);
 }
+// raw coefficient words (lo, hi; hi = 0 for cw = 1) at any index: zero at or
+// beyond kc, last one masked
+__device__ __forceinline__ uint2 coef_raw_at(const OpView& o, int gi) {
+  uint2 w = make_uint2(0u, 0u);
+  if (gi < o.kc) {
+    if (o.cw == 2) {
+      w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+    } else {
+      w.x = __ldg(o.src + gi);
+    }
+    if (gi == o.kc - 1) {
+      w.x &= o.mlo;
+      w.y &= o.mhi;
+    }
+  }
+  return w;
+}
+
 // any coefficient index: zero at or beyond kc, last one masked
 template <int P>
 __device__ __forceinline__ u32 coef_at(const OpView& o, int gi) {
@@ -106,6 +126,48 @@ __device__ __forceinline__ FwdIdx fwd_idx(const ConvJob& job, int lct) {
   r.op = (int)(w / tc);
   r.tile = (int)(w - (unsigned)r.op * tc);
   return r;
+}
+
+// Operand staging for the all-primes forward column kernel: rows [0, rows) x
+// CT columns of raw coefficients (uint2: lo, hi; hi = 0 for cw = 1) at
+// stage[row * CT + t] via cp.async, so the whole tile's loads are in flight at
+// once and are then reused by every prime.  Coefficients >= kc are zero, the
+// last one is masked.
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((u32)__cvta_generic_to_shared(s)),
+               "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((u32)__cvta_generic_to_shared(s)),
+               "l"(g));
+}
+__device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, int rows, int lct,
+                                              int lgC, int c0) {
+  const int CT = 1 << lct;
+  for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
+    const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
+    if (gi < ov.kc - 1) {
+      if (ov.cw == 2) {
+        cp_async8(stage + e, ov.src + 2 * gi);
+      } else {
+        cp_async4(stage + e, ov.src + gi);
+        reinterpret_cast<u32*>(stage + e)[1] = 0u;
+      }
+    } else {
+      stage[e] = coef_raw_at(ov, gi);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+}
+
+// staged raw coefficient (row, t) -> residue in [0, 2p); rows >= srows are zero
+template <int P>
+__device__ __forceinline__ u32 coef_staged(const uint2* stage, int row, int t, int lct, int srows,
+                                           int cw) {
+  if (row >= srows) return 0u;
+  const uint2 w = stage[(row << lct) + t];
+  return coef_red<P>(w.x, w.y, cw);
 }
 
 // conv kernels run one prime per grid index IDX (job.np of them).  Kernels
@@ -387,9 +449,10 @@ __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int ln
 // smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
 // broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
 // scaled residues.
-template <int P, int LGR, int LGC>
+template <int P, int LGR, int LGC, bool STAGED = false>
 __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
-                                             int b, int op, int tile) {
+                                             int b, int op, int tile,
+                                             const uint2* stage = nullptr) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
@@ -420,7 +483,24 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
       const int t = task & (CT - 1), o = task >> lct;
       const int col = c0 + t;
       u32 v[1][1 << RS0];
-      if (half) {
+      if constexpr (STAGED) {  // raw coefficients of rows o + k 2^SLO0 from the staged tile
+        constexpr int NK = 1 << RS0;
+        if (half) {
+#pragma unroll
+          for (int k = 0; k < NK / 2; ++k) {
+            const uint2 w = stage[((o + (k << SLO0)) << lct) + t];
+            v[0][k] = coef_red<P>(w.x, w.y, ov.cw);
+          }
+          dif_rt_half<P, RS0, SLO0>(v, twf + o);
+        } else {
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            const uint2 w = stage[((o + (k << SLO0)) << lct) + t];
+            v[0][k] = coef_red<P>(w.x, w.y, ov.cw);
+          }
+          dif_rt<P, RS0, SLO0, 1>(v, twf + o);
+        }
+      } else if (half) {
         const int g0 = (o << lgC) + col;
         constexpr int kTop = ((1 << (RS0 - 1)) - 1) << (SLO0 + lgC);
         if (g0 + kTop < ilast) {  // every coefficient of the task is valid and unmasked
@@ -589,9 +669,10 @@ __device__ __forceinline__ void colm_pass(u32* smem, int lct, const uint2* __res
   }
 }
 
-template <int P, int M, int LGR2, int LGC>
+template <int P, int M, int LGR2, int LGC, bool STAGED = false>
 __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
-                                             int b, int op, int tile) {
+                                             int b, int op, int tile,
+                                             const uint2* stage = nullptr, int srows = 0) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR2);
   constexpr int R2 = 1 << LGR2, T2 = sm_len(LGR2);
@@ -620,7 +701,8 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
         u32 a[M];
 #pragma unroll
         for (int s = 0; s < M; ++s) {
-          a[s] = coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
+          a[s] = STAGED ? coef_staged<P>(stage, j + s * R2, t, lct, srows, ov.cw)
+                     : coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
         }
         radix_m<P, M, false>(a);
 #pragma unroll
@@ -646,7 +728,8 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
     u32 a[M];
 #pragma unroll
     for (int s = 0; s < M; ++s) {
-      a[s] = coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
+      a[s] = STAGED ? coef_staged<P>(stage, j + s * R2, t, lct, srows, ov.cw)
+                     : coef_at<P>(ov, ((j + s * R2) << lgC) + c0 + t);
     }
     radix_m<P, M, false>(a);
 #pragma unroll
@@ -792,6 +875,58 @@ __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab,
   PAB_PRIME_SWITCH(PAB_B, ix.prime)
 #undef PAB_B
 }
+// All primes of one (block, operand, column tile) per CTA: the raw operand tile
+// is staged once (cp.async) and transformed for each prime in turn.  1-D grid:
+// tile fastest, then operand, then block.  Dynamic smem: the transform panel
+// plus the stage (rows x CT x 8 bytes).
+template <int LGR, int LGC>
+__global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab, int lct) {
+  extern __shared__ u32 smem[];
+  const int CT = 1 << lct;
+  const unsigned tc = 1u << (LGC - lct);
+  const int tile = (int)(blockIdx.x % tc);
+  const int rest = (int)(blockIdx.x / tc);
+  const int op = rest & 1, b = rest >> 1;
+  const OpView ov = op_view(job, op, b);
+  const bool half = ov.kc <= (job.L >> 1);
+  const int rows = half ? (1 << (LGR - 1)) : (1 << LGR);
+  uint2* stage = reinterpret_cast<uint2*>(smem + sm_len(LGR) * CT);
+  stage_operand(ov, stage, rows, lct, LGC, tile << lct);
+  sfor<kNumPrimes>([&](auto pc) {
+    constexpr int P = decltype(pc)::value;
+    if (P < job.np) {
+      col_fwd_body<P, LGR, LGC, true>(job, tab, lct, b, op, tile, stage);
+      __syncthreads();  // the next prime reuses the transform panel
+    }
+  });
+}
+
+// Mixed radix, all primes per CTA: stages the operand rows holding nonzero
+// coefficients (row < ceil(kc / C)) once, then each prime's radix-M + pow2
+// column DFT reads them from smem.
+template <int M, int LGR2, int LGC>
+__global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int lct) {
+  extern __shared__ u32 smem[];
+  const int CT = 1 << lct;
+  const unsigned tc = 1u << (LGC - lct);
+  const int tile = (int)(blockIdx.x % tc);
+  const int rest = (int)(blockIdx.x / tc);
+  const int op = rest & 1, b = rest >> 1;
+  const OpView ov = op_view(job, op, b);
+  const int R = M << LGR2;
+  int rows = (ov.kc + (1 << LGC) - 1) >> LGC;
+  if (rows > R) rows = R;
+  uint2* stage = reinterpret_cast<uint2*>(smem + M * sm_len(LGR2) * CT);
+  stage_operand(ov, stage, rows, lct, LGC, tile << lct);
+  sfor<kNumPrimes>([&](auto pc) {
+    constexpr int P = decltype(pc)::value;
+    if (P < job.np) {
+      colm_fwd_body<P, M, LGR2, LGC, true>(job, tab, lct, b, op, tile, stage, rows);
+      __syncthreads();  // the next prime reuses the transform panel
+    }
+  });
+}
+
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
 #define PAB_B(P_) col_inv_body<P_, LGR, LGC>(job, tab, lct);
@@ -815,6 +950,8 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
     k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<R_, R_> : nullptr;                  \
     k.col_fwd1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd<R_, C1_> : nullptr;     \
     k.col_inv1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_inv<R_, C1_> : nullptr;     \
+    k.col_fwd_all = (LG >= 6) ? (ConvKernel)k_col_fwd_all<R_, R_> : nullptr;          \
+    k.col_fwd_all1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd_all<R_, C1_> : nullptr; \
     constexpr int M2_ = LG >= 3 && LG <= 10 ? LG : 3;                                 \
     const bool mx_ = LG >= 3 && LG <= 10;                                             \
     constexpr int CA_ = M2_ + 2 <= 12 ? M2_ + 2 : 12;                                  \
@@ -826,6 +963,12 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
     k.colm_fwd[1][0] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CA_> : nullptr;           \
     k.colm_fwd[1][1] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CB_> : nullptr;           \
     k.colm_fwd[1][2] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CC_> : nullptr;           \
+    k.colm_fwd_all[0][0] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CA_> : nullptr;   \
+    k.colm_fwd_all[0][1] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CB_> : nullptr;   \
+    k.colm_fwd_all[0][2] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CC_> : nullptr;   \
+    k.colm_fwd_all[1][0] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CA_> : nullptr;   \
+    k.colm_fwd_all[1][1] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CB_> : nullptr;   \
+    k.colm_fwd_all[1][2] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CC_> : nullptr;   \
     k.colm_inv[0][0] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CA_> : nullptr;           \
     k.colm_inv[0][1] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CB_> : nullptr;           \
     k.colm_inv[0][2] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CC_> : nullptr;           \

@@ -818,6 +818,18 @@ static ConvKernel colm_kernel(int m, int lgR, int lgC, bool inv) {
   const int i = m == 3 ? 0 : 1;
   return inv ? k.colm_inv[i][dc] : k.colm_fwd[i][dc];
 }
+static ConvKernel colm_fwd_all_kernel(int m, int lgR, int lgC) {
+  const int dc = lgC - lgR - 2;
+  if (lgR < 3 || lgR > 10 || (m != 3 && m != 5) || dc < 0 || dc > 2 || lgC > 12) return nullptr;
+  return conv_for(lgR).colm_fwd_all[m == 3 ? 0 : 1][dc];
+}
+static ConvKernel col_fwd_all_kernel(int lgR, int lgC) {
+  if (lgR < 6) return nullptr;
+  const ConvKernels k = conv_for(lgR);
+  if (lgC == lgR) return k.col_fwd_all;
+  if (lgC == lgR + 1) return k.col_fwd_all1;
+  return nullptr;
+}
 static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
   if (lgR < 6) return nullptr;
   const ConvKernels k = conv_for(lgR);
@@ -869,7 +881,36 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     }();
     if (force_ci && job.m > 1) ct_threads = force_ci;
   }
-  {
+  // Forward column pass: all primes per CTA from one staged operand tile (loads
+  // once, reused five times) where measured faster -- pow2 columns up to 2^8,
+  // mixed radix up to 2^7 per sub-column; longer columns stage too many rows
+  // per CTA (occupancy) and keep the per-prime kernel with its L2-chunked grid.
+  // PAB_FWD_ALL=0/1 forces either (tests, experiments).
+  static const int fwd_env = [] {
+    const char* e = getenv("PAB_FWD_ALL");
+    return e ? atoi(e) : -1;
+  }();
+  const bool fwd_all = fwd_env >= 0 ? fwd_env != 0 : job.lgR <= (job.m == 1 ? 8 : 7);
+  const long long kcmax = ((job.kA > job.kX ? job.kA : job.kX) + job.cw - 1) / job.cw;
+  const unsigned ctas_all = (1u << (job.lgC - lct)) * 2u * (unsigned)job.batch;
+  if (job.m == 1 && fwd_all) {
+    const int rows = kcmax <= (job.L >> 1) ? (int)(R >> 1) : (int)R;
+    const size_t sma = smc + (size_t)rows * (1u << lct) * 8;
+    prof::Scope ps_("k_col_fwd", st);
+    col_fwd_all_kernel(job.lgR, job.lgC)<<<ctas_all, threads, sma, st>>>(job, tab, lct);
+  } else if (job.m > 1 && fwd_all) {
+    static const int dl = [] {  // development override: narrower tiles for the staged pass
+      const char* e = getenv("PAB_COLM_ALL_DLCT");
+      return e ? atoi(e) : 1;
+    }();
+    const int lcta = lct - dl < 2 ? 2 : lct - dl;
+    long long rows = (kcmax + (1ll << job.lgC) - 1) >> job.lgC;
+    if (rows > R) rows = R;
+    const size_t sma = (size_t)job.m * sm_len(job.lgR) * (1u << lcta) * 4 + (size_t)rows * (1u << lcta) * 8;
+    const unsigned ctas = (1u << (job.lgC - lcta)) * 2u * (unsigned)job.batch;
+    prof::Scope ps_("k_col_fwd", st);
+    colm_fwd_all_kernel(job.m, job.lgR, job.lgC)<<<ctas, cf_threads, sma, st>>>(job, tab, lcta);
+  } else {
     prof::Scope ps_("k_col_fwd", st);
     // ~32 MiB of operand words per chunk (L2-resident across the prime sweeps)
     ConvJob jf = job;
@@ -926,11 +967,15 @@ void set_kernel_attrs() {
       for (int dc = 0; dc < 2; ++dc) {
         ConvKernel c = col_kernel(lg, lg + dc, s != 0);
         if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        ConvKernel a = s ? nullptr : col_fwd_all_kernel(lg, lg + dc);
+        if (a) cudaFuncSetAttribute(a, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       }
       for (int m = 3; m <= 5; m += 2)
         for (int dc = 2; dc <= 4; ++dc) {
           ConvKernel c = colm_kernel(m, lg, lg + dc, s != 0);
           if (c) cudaFuncSetAttribute(c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          ConvKernel a = s ? nullptr : colm_fwd_all_kernel(m, lg, lg + dc);
+          if (a) cudaFuncSetAttribute(a, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         }
     }
   }
