@@ -415,6 +415,52 @@ def step_roofline(n: int, r: int, blocks: int, ms_step: float) -> dict | None:
             "roofline_mbps": round(blocks * n / t_roof / 1e3, 1)}
 
 
+def baseline_roofline(n: int, r: int, blocks: int, ms_step: float) -> dict | None:
+    """The BASELINE.md §4 roofline: the canonical G16 design (Goldilocks prime,
+    16-bit coefficients, 2 HBM passes per NTT) at the measured int peak and HBM
+    bandwidth -- the north star's "NTT roofline" as frozen before optimising.
+    This design does fewer ops than G16, so its frac can exceed 1; step_roofline
+    is the same ratio against this design's own op count."""
+    pk = peaks()
+    if not pk["int_tops"]:
+        return None
+    K = -(-n // 16)
+    L = 1 << (2 * K - 2).bit_length()
+    lg = L.bit_length() - 1
+    ops = 3 * (L // 2) * lg * 26 + 16 * L + 12 * K
+    byts = 80 * L + 3 * n // 8 + r // 8
+    t_int = blocks * ops / (pk["int_tops"] * 1e12) * 1e3
+    t_hbm = blocks * byts / (pk["hbm_gbs"] * 1e9) * 1e3
+    t_roof = max(t_int, t_hbm)
+    return {"design": "G16 (BASELINE.md §4)", "L": L, "int_ops_per_block": ops,
+            "hbm_bytes_per_block": byts, "t_roof_ms": round(t_roof, 4),
+            "measured_ms": round(ms_step, 4), "frac": round(t_roof / ms_step, 4),
+            "bound": "int" if t_int >= t_hbm else "hbm",
+            "roofline_mbps": round(blocks * n / t_roof / 1e3, 1)}
+
+
+def dropin_timing(n: int, r: int, calls: int = 10) -> dict:
+    """Timing scope (iii) of SURVEY §8d: the drop-in Python call the reference's
+    users make, pa.compress(BitBlock, HashSeed, r), including int <-> bytes and
+    the host <-> device copies, one block per call (median of `calls`)."""
+    import paper_1910_04429_b200 as pab
+    from paper_1910_04429_b200 import workloads
+
+    x = workloads.block_inputs(n, 0)[0]
+    xb = pab.import_block(x, n)
+    seed = pab.gen_seed(n, pab.derive_block_seed(0, n))  # the reference's derivation (untimed)
+    pab.compress(xb, seed, r)
+    ts = []
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        pab.compress(xb, seed, r)
+        ts.append(time.perf_counter() - t0)
+    ms = sorted(ts)[len(ts) // 2] * 1e3
+    return {"value": round(n / (ms * 1e-3) / 1e6, 1), "unit": "Mbps", "ms_per_call": round(ms, 3),
+            "scope": "pa.compress(BitBlock, HashSeed, r): one n=%d block per call, incl. "
+                     "int<->bytes and host<->device copies (median of %d)" % (n, calls)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -472,7 +518,9 @@ def main():
     roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk,
                                  workload=cfg["name"] if res["eng"].chunk == 1024 else None)
     step_roof = step_roofline(n, r, per_rank, res["ms_step"])
+    base_roof = baseline_roofline(n, r, per_rank, res["ms_step"])
     launches = sum(v[0] for v in res["prof"].values())
+    dropin = dropin_timing(n, r) if rank == 0 and world == 1 and not args.no_extra else None
 
     extra = {}
     cpu = None
@@ -501,7 +549,7 @@ def main():
                        "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
                              % (3 * per_rank * ((n + 7) // 8) / 1e6)},
             "e2e": res["e2e"], "gpu_launches": launches, "roofline": roof,
-            "step_roofline": step_roof,
+            "step_roofline": step_roof, "baseline_roofline": base_roof, "dropin": dropin,
             "kernels": kernels, "clocks": res["clocks"], "cpu_baseline": cpu,
         }
         if extra:
@@ -533,7 +581,8 @@ def side_1e8(args, dist) -> dict:
     return {"workload": "C5 subset: %d blocks/rank, n=1e8, r=5e7" % B,
             "value": round(world * B * n / (ms_step * 1e-3) / 1e6, 1), "unit": "Mbps",
             "ms_per_step": round(ms_step, 3), "roofline": roof,
-            "step_roofline": step_roofline(n, r, B, ms_step), "kernels": kernels}
+            "step_roofline": step_roofline(n, r, B, ms_step),
+            "baseline_roofline": baseline_roofline(n, r, B, ms_step), "kernels": kernels}
 
 
 if __name__ == "__main__":
