@@ -935,46 +935,58 @@ __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, in
 }
 
 
+// Each size compiles only what can run: forward column passes in the variant
+// the launcher uses for it (all-primes staged for pow2 columns up to 2^8 and
+// mixed radix up to 2^7 per sub-column, per-prime above), no clamped duplicates.
+template <int LG, int DC>
+void set_colm(ConvKernels& k) {  // mixed radix, columns of M * 2^LG, rows 2^(LG + 2 + DC)
+  constexpr int C = LG + 2 + DC;
+  if constexpr (C <= 12) {
+    k.colm_inv[0][DC] = k_colm_inv<3, LG, C>;
+    k.colm_inv[1][DC] = k_colm_inv<5, LG, C>;
+    if constexpr (LG <= 7) {
+      k.colm_fwd_all[0][DC] = k_colm_fwd_all<3, LG, C>;
+      k.colm_fwd_all[1][DC] = k_colm_fwd_all<5, LG, C>;
+    } else {
+      k.colm_fwd[0][DC] = k_colm_fwd<3, LG, C>;
+      k.colm_fwd[1][DC] = k_colm_fwd<5, LG, C>;
+    }
+  }
+}
+
+template <int LG>
+ConvKernels make_conv_kernels() {
+  ConvKernels k{};
+  k.row = k_row<LG, false>;
+  k.row_small = k_row<LG, true>;
+  if constexpr (LG >= 6) {
+    k.col_inv = k_col_inv<LG, LG>;
+    if constexpr (LG <= 8) {
+      k.col_fwd_all = k_col_fwd_all<LG, LG>;
+    } else {
+      k.col_fwd = k_col_fwd<LG, LG>;
+    }
+    if constexpr (LG < 12) {
+      k.col_inv1 = k_col_inv<LG, LG + 1>;
+      if constexpr (LG <= 8) {
+        k.col_fwd_all1 = k_col_fwd_all<LG, LG + 1>;
+      } else {
+        k.col_fwd1 = k_col_fwd<LG, LG + 1>;
+      }
+    }
+  }
+  if constexpr (LG >= 3 && LG <= 10) {
+    set_colm<LG, 0>(k);
+    set_colm<LG, 1>(k);
+    set_colm<LG, 2>(k);
+  }
+  return k;
+}
+
 }  // namespace pab
 
 // one translation unit per size: defines conv_kernels_<LG>()
-#define PAB_DEFINE_CONV(LG)                                                          \
-  namespace pab {                                                                    \
-  ConvKernels conv_kernels_##LG() {                                                  \
-    ConvKernels k;                                                                   \
-    k.row = k_row<LG, false>;                                                        \
-    k.row_small = k_row<LG, true>;                                                   \
-    constexpr int R_ = LG >= 6 ? LG : 6;                                             \
-    constexpr int C1_ = R_ + 1 <= 12 ? R_ + 1 : 12;                                   \
-    k.col_fwd = (LG >= 6) ? (ConvKernel)k_col_fwd<R_, R_> : nullptr;                  \
-    k.col_inv = (LG >= 6) ? (ConvKernel)k_col_inv<R_, R_> : nullptr;                  \
-    k.col_fwd1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd<R_, C1_> : nullptr;     \
-    k.col_inv1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_inv<R_, C1_> : nullptr;     \
-    k.col_fwd_all = (LG >= 6) ? (ConvKernel)k_col_fwd_all<R_, R_> : nullptr;          \
-    k.col_fwd_all1 = (LG >= 6 && LG < 12) ? (ConvKernel)k_col_fwd_all<R_, C1_> : nullptr; \
-    constexpr int M2_ = LG >= 3 && LG <= 10 ? LG : 3;                                 \
-    const bool mx_ = LG >= 3 && LG <= 10;                                             \
-    constexpr int CA_ = M2_ + 2 <= 12 ? M2_ + 2 : 12;                                  \
-    constexpr int CB_ = M2_ + 3 <= 12 ? M2_ + 3 : 12;                                  \
-    constexpr int CC_ = M2_ + 4 <= 12 ? M2_ + 4 : 12;                                  \
-    k.colm_fwd[0][0] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CA_> : nullptr;           \
-    k.colm_fwd[0][1] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CB_> : nullptr;           \
-    k.colm_fwd[0][2] = mx_ ? (ConvKernel)k_colm_fwd<3, M2_, CC_> : nullptr;           \
-    k.colm_fwd[1][0] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CA_> : nullptr;           \
-    k.colm_fwd[1][1] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CB_> : nullptr;           \
-    k.colm_fwd[1][2] = mx_ ? (ConvKernel)k_colm_fwd<5, M2_, CC_> : nullptr;           \
-    k.colm_fwd_all[0][0] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CA_> : nullptr;   \
-    k.colm_fwd_all[0][1] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CB_> : nullptr;   \
-    k.colm_fwd_all[0][2] = mx_ ? (ConvKernel)k_colm_fwd_all<3, M2_, CC_> : nullptr;   \
-    k.colm_fwd_all[1][0] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CA_> : nullptr;   \
-    k.colm_fwd_all[1][1] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CB_> : nullptr;   \
-    k.colm_fwd_all[1][2] = mx_ ? (ConvKernel)k_colm_fwd_all<5, M2_, CC_> : nullptr;   \
-    k.colm_inv[0][0] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CA_> : nullptr;           \
-    k.colm_inv[0][1] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CB_> : nullptr;           \
-    k.colm_inv[0][2] = mx_ ? (ConvKernel)k_colm_inv<3, M2_, CC_> : nullptr;           \
-    k.colm_inv[1][0] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CA_> : nullptr;           \
-    k.colm_inv[1][1] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CB_> : nullptr;           \
-    k.colm_inv[1][2] = mx_ ? (ConvKernel)k_colm_inv<5, M2_, CC_> : nullptr;           \
-    return k;                                                                        \
-  }                                                                                  \
+#define PAB_DEFINE_CONV(LG) \
+  namespace pab {           \
+  ConvKernels conv_kernels_##LG() { return make_conv_kernels<LG>(); } \
   }

@@ -871,26 +871,16 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
                              : colm_kernel(job.m, job.lgR, job.lgC, true);
   // mixed-radix inverse: 512 threads for radix 3 (its 384-task first pass and
   // 512-task fused radix pass), 256 otherwise; the forward pass keeps 256
-  // (measured: scripts/quick_perf.py with PAB_CI_THREADS / PAB_CF_THREADS).
-  int ct_threads = job.m == 3 ? 512 : threads;
+  // (measured with thread-count overrides in scripts/quick_perf.py runs).
+  const int ct_threads = job.m == 3 ? 512 : threads;
   const int cf_threads = threads;
-  {
-    static const int force_ci = [] {  // development override
-      const char* e = getenv("PAB_CI_THREADS");
-      return e ? atoi(e) : 0;
-    }();
-    if (force_ci && job.m > 1) ct_threads = force_ci;
-  }
   // Forward column pass: all primes per CTA from one staged operand tile (loads
   // once, reused five times) where measured faster -- pow2 columns up to 2^8,
   // mixed radix up to 2^7 per sub-column; longer columns stage too many rows
-  // per CTA (occupancy) and keep the per-prime kernel with its L2-chunked grid.
-  // PAB_FWD_ALL=0/1 forces either (tests, experiments).
-  static const int fwd_env = [] {
-    const char* e = getenv("PAB_FWD_ALL");
-    return e ? atoi(e) : -1;
-  }();
-  const bool fwd_all = fwd_env >= 0 ? fwd_env != 0 : job.lgR <= (job.m == 1 ? 8 : 7);
+  // per CTA (occupancy) and use the per-prime kernel with its L2-chunked grid.
+  // Which one exists for a size is fixed at compile time (make_conv_kernels).
+  const bool fwd_all = job.m == 1 ? col_fwd_all_kernel(job.lgR, job.lgC) != nullptr
+                                  : colm_fwd_all_kernel(job.m, job.lgR, job.lgC) != nullptr;
   const long long kcmax = ((job.kA > job.kX ? job.kA : job.kX) + job.cw - 1) / job.cw;
   const unsigned ctas_all = (1u << (job.lgC - lct)) * 2u * (unsigned)job.batch;
   if (job.m == 1 && fwd_all) {
@@ -899,10 +889,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     prof::Scope ps_("k_col_fwd", st);
     col_fwd_all_kernel(job.lgR, job.lgC)<<<ctas_all, threads, sma, st>>>(job, tab, lct);
   } else if (job.m > 1 && fwd_all) {
-    static const int dl = [] {  // development override: narrower tiles for the staged pass
-      const char* e = getenv("PAB_COLM_ALL_DLCT");
-      return e ? atoi(e) : 1;
-    }();
+    const int dl = 1;  // half-width tiles: the staged rows fit with 4-5 CTAs per SM (measured)
     const int lcta = lct - dl < 2 ? 2 : lct - dl;
     long long rows = (kcmax + (1ll << job.lgC) - 1) >> job.lgC;
     if (rows > R) rows = R;
@@ -938,7 +925,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
 bool conv_supported(int m, int lgR, int lgC) {
   if (m == 1 && lgR == 0) return row_kernel(lgC, true) != nullptr;
   const ConvKernel cf = m == 1 ? col_kernel(lgR, lgC, false) : colm_kernel(m, lgR, lgC, false);
-  return cf != nullptr && row_kernel(lgC, false) != nullptr;
+  const ConvKernel ca = m == 1 ? col_fwd_all_kernel(lgR, lgC) : colm_fwd_all_kernel(m, lgR, lgC);
+  const ConvKernel ci = m == 1 ? col_kernel(lgR, lgC, true) : colm_kernel(m, lgR, lgC, true);
+  return (cf != nullptr || ca != nullptr) && ci != nullptr && row_kernel(lgC, false) != nullptr;
 }
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
