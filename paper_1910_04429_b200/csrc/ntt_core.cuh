@@ -84,12 +84,12 @@ __host__ __device__ constexpr PassPlan pass_plan(int lg) {
   } else if (rem == 5) {
     parts[np++] = 3;
     parts[np++] = 2;
-  } else if (rem == 6) {
-    parts[np++] = 3;
-    parts[np++] = 3;
-  } else {  // rem == 7 (lg 12)
-    parts[np++] = 3;
+  } else if (rem == 6) {  // lg 11, 12: the heavier pass first (measured: k_row -5%)
     parts[np++] = 4;
+    parts[np++] = 2;
+  } else {  // rem == 7 (lg 12)
+    parts[np++] = 4;
+    parts[np++] = 3;
   }
   int s = lg;
   for (int i = 0; i < np; ++i) {
