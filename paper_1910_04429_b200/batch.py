@@ -80,41 +80,61 @@ class HashEngine:
         return out
 
     def hash_host(self, x: torch.Tensor, c: torch.Tensor, d: torch.Tensor,
-                  out: torch.Tensor | None = None, streams: int = 2,
+                  out: torch.Tensor | None = None, streams: int = 3,
                   chunk: int | None = None) -> torch.Tensor:
         """End-to-end from (pinned) host tensors: H2D, hash, D2H, overlapped.
 
-        Chunks of blocks rotate over `streams` CUDA streams so the copy of
-        chunk i+1 overlaps the hashing of chunk i.  Returns host [batch, ceil(r/8)].
+        A triple-buffered pipeline: one stream each for H2D, hashing and D2H,
+        `streams` device buffer slots, and per-slot events so the copy engines
+        only wait for a slot to be free (the H2D of chunk i+slots waits for the
+        hashing of chunk i to have read its inputs).  The slot events persist
+        across calls, so back-to-back calls overlap as well.  Returns host
+        [batch, ceil(r/8)] (complete once the caller's current stream is synced).
         """
         b = x.shape[0]
         if out is None:
             out = torch.empty((b, self.rbytes), dtype=torch.uint8, pin_memory=True)
         chunk = chunk or self.chunk
-        sts = self._streams(streams)
-        bufs = self._io_buffers(len(sts), chunk)
+        nslots = max(1, streams)
+        s_in, s_comp, s_out = self._pipe_streams()
+        bufs = self._io_buffers(nslots, chunk)
+        ev = self._slot_events(nslots)
         cur = torch.cuda.current_stream(self.device)
-        for s in sts:
+        for s in (s_in, s_comp, s_out):
             s.wait_stream(cur)
         for i, b0 in enumerate(range(0, b, chunk)):
-            k = i % len(sts)
-            st = sts[k]
+            k = i % nslots
             dx, dc, dd, dout = bufs[k]
             nb = min(chunk, b - b0)
-            with torch.cuda.stream(st):
+            s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
+            with torch.cuda.stream(s_in):
                 dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
                 dc[:nb].copy_(c[b0:b0 + nb], non_blocking=True)
                 dd[:nb].copy_(d[b0:b0 + nb], non_blocking=True)
-                self.hash_device(dx[:nb], dc[:nb], dd[:nb], dout[:nb], stream=st)
+                ev["in"][k].record(s_in)
+            s_comp.wait_event(ev["in"][k])
+            s_comp.wait_event(ev["out"][k])      # slot k's output drained
+            self.hash_device(dx[:nb], dc[:nb], dd[:nb], dout[:nb], stream=s_comp)
+            ev["comp"][k].record(s_comp)
+            s_out.wait_event(ev["comp"][k])
+            with torch.cuda.stream(s_out):
                 out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
-        for s in sts:
+                ev["out"][k].record(s_out)
+        for s in (s_in, s_comp, s_out):
             cur.wait_stream(s)
         return out
 
-    def _streams(self, k: int):
-        if not hasattr(self, "_sts") or len(self._sts) != k:
-            self._sts = [torch.cuda.Stream(self.device) for _ in range(k)]
-        return self._sts
+    def _pipe_streams(self):
+        if not hasattr(self, "_pipe"):
+            self._pipe = tuple(torch.cuda.Stream(self.device) for _ in range(3))
+        return self._pipe
+
+    def _slot_events(self, k: int):
+        if getattr(self, "_ev_k", None) != k:
+            mk = lambda: [torch.cuda.Event() for _ in range(k)]  # noqa: E731
+            self._ev = {"in": mk(), "comp": mk(), "out": mk()}
+            self._ev_k = k
+        return self._ev
 
     def _io_buffers(self, k: int, chunk: int):
         key = (k, chunk)
