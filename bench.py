@@ -352,20 +352,24 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
     return res
 
 
-def ncu_traffic(workload: str | None) -> dict:
-    """Per-launch DRAM bytes of each kernel from the committed ncu capture of this workload."""
+def ncu_traffic(workload: str | None, batch: int | None = None) -> dict:
+    """Per-launch DRAM bytes of each kernel from the committed ncu capture of this
+    workload, if it was captured at the same blocks per launch."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not workload or not os.path.exists(path):
         return {}
     with open(path) as f:
-        return json.load(f).get("workloads", {}).get(workload, {})
+        rec = json.load(f).get("workloads", {}).get(workload, {})
+    if batch is not None and rec.get("batch") not in (None, batch):
+        return {}
+    return {k: v for k, v in rec.items() if k != "batch"}
 
 
 def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int,
                  workload: str | None = None) -> tuple[dict, dict]:
     model = kernel_model(n, r, blocks)
     pk = peaks()
-    traffic = ncu_traffic(workload)
+    traffic = ncu_traffic(workload, blocks)
     total = sum(v[1] for v in prof.values()) or 1.0
     kernels = {}
     for name, (cnt, ms) in prof.items():
@@ -516,7 +520,7 @@ def main():
     res = run_ours(args, cfg, rank, local_rank, world)
     n, r, per_rank = res["n"], res["r"], res["per_rank"]
     roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk,
-                                 workload=cfg["name"] if res["eng"].chunk == 1024 else None)
+                                 workload=cfg["name"])
     step_roof = step_roofline(n, r, per_rank, res["ms_step"])
     base_roof = baseline_roofline(n, r, per_rank, res["ms_step"])
     launches = sum(v[0] for v in res["prof"].values())
