@@ -684,6 +684,17 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
   u32* dst = job.buf + (((long long)b * 2 + op) * job.np + P) * L;
   const uint2* twf = tab.stw + (P * 2 + 0) * kTwN;
   const uint2* trad = tab.trad + (P * 2 + 0) * tab.tstride;
+  if constexpr (!STAGED) {  // L2 prefetch of this CTA's operand lines (first use is the radix pass)
+    const int rows = min((ov.kc + (1 << LGC) - 1) >> LGC, M << LGR2);
+    const int lpr = (CT * ov.cw * 4 + 127) >> 7;  // 128-byte lines per row segment
+    const char* end = reinterpret_cast<const char*>(ov.src + (size_t)ov.kc * ov.cw);
+    for (int i = threadIdx.x; i < rows * lpr; i += blockDim.x) {
+      const int row = i / lpr, ln = i - row * lpr;
+      const char* p =
+          reinterpret_cast<const char*>(ov.src + (size_t)((row << LGC) + c0) * ov.cw) + (ln << 7);
+      if (p < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    }
+  }
   constexpr bool FUSE = PP.n >= 2 && M * (1 << PP.rs[0]) <= 32;  // register budget
   if constexpr (FUSE) {
     // radix-M stage fused with the first pow2 pass (when M * 2^RS0 <= 32 values fit in
