@@ -940,7 +940,9 @@ void launch_carry(const ConvJob& job, cudaStream_t st) {
     const char* e = getenv("PAB_CARRY_MODE");
     return e ? (e[0] == 's' ? 1 : 2) : 0;
   }();
-  const bool seq = job.tiles == 1 || (force ? force == 1 : job.batch >= 2 * 148);
+  // look-back everywhere (batch-major grid, measured faster than one CTA per
+  // block walking its tiles even at 1024 blocks); sequential for one-tile blocks
+  const bool seq = job.tiles == 1 || force == 1;
   const dim3 grid = seq ? dim3(1, job.batch) : dim3(job.batch, job.tiles);
   if (job.cw == 2) {
     if (seq) k_carry_seq<2><<<grid, kCarryThreads, 0, st>>>(job);

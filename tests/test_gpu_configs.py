@@ -114,8 +114,8 @@ def test_prefix_property_and_offset_linearity():
 
 @pytest.mark.parametrize("batch", [1, 300])
 def test_unaligned_shift_across_tiles(batch, coef_words):
-    # (n - r) % 32 != 0 with outputs spanning many carry tiles, in both the
-    # look-back (few blocks) and the sequential (many blocks) carry modes
+    # (n - r) % 32 != 0 with outputs spanning many carry tiles, one block and
+    # many blocks in flight (look-back carry)
     n = 300_007 if batch > 1 else 3_000_013
     rng = np.random.default_rng(21 + batch)
     nb = (n + 7) // 8
@@ -224,3 +224,37 @@ def test_exhaustive_alpha6_on_gpu_batched():
         out = HashEngine(alpha, beta, max_batch=4096).hash_device(x, c, d).cpu().numpy()[:, 0]
         want = ((cs_ * xs_ + ds_) % 64) >> (alpha - beta)
         assert np.array_equal(out, want.reshape(-1).astype(np.uint8))
+
+
+def test_sequential_carry_mode_matches_oracle():
+    # the one-CTA-per-block carry (production only for one-tile blocks) across
+    # many tiles, forced through its development switch in a fresh process
+    import os
+    import subprocess
+    import sys
+
+    code = """
+import numpy as np, torch, oracle
+from paper_1910_04429_b200.batch import HashEngine
+from paper_1910_04429_b200 import _native
+for cw in (2, 1):
+    _native.force_coef_words(cw)
+    for n, r, B in ((300_007, 123_457, 3), (2_000_000, 999_999, 2)):
+        rng = np.random.default_rng(n + cw)
+        nb = (n + 7) // 8
+        arr = rng.integers(0, 256, size=(3, B, nb), dtype=np.uint8)
+        if n % 8:
+            arr[:, :, -1] &= (1 << (n % 8)) - 1
+        arr[1, :, 0] |= 1
+        out = HashEngine(n, r, max_batch=B).hash_device(*(torch.from_numpy(a).cuda() for a in arr))
+        out = out.cpu().numpy()
+        for i in range(B):
+            want = oracle.compress(*(arr[j, i].tobytes() for j in range(3)), n, r)
+            assert out[i].tobytes() == want, (cw, n, i)
+print("SEQ_OK")
+"""
+    env = dict(os.environ, PAB_CARRY_MODE="seq")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0 and "SEQ_OK" in res.stdout, res.stderr[-2000:]
