@@ -647,7 +647,7 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
     }
   }
   const u32 cout = cf_apply(agg, tile_cin);
-  __syncthreads();  // smem reuse by the next tile
+  if (!LOOKBACK) __syncthreads();  // smem reuse by the next tile (look-back CTAs own one tile)
   return cout;
 }
 
