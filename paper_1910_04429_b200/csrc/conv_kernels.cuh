@@ -452,7 +452,8 @@ __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int ln
 template <int P, int LGR, int LGC, bool STAGED = false>
 __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
                                              int b, int op, int tile,
-                                             const uint2* stage = nullptr) {
+                                             const uint2* stage = nullptr,
+                                             const uint2* s_tw = nullptr) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
@@ -491,14 +492,14 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
             const uint2 w = stage[((o + (k << SLO0)) << lct) + t];
             v[0][k] = coef_red<P>(w.x, w.y, ov.cw);
           }
-          dif_rt_half<P, RS0, SLO0>(v, twf + o);
+          dif_rt_half<P, RS0, SLO0, true>(v, s_tw + o);
         } else {
 #pragma unroll
           for (int k = 0; k < NK; ++k) {
             const uint2 w = stage[((o + (k << SLO0)) << lct) + t];
             v[0][k] = coef_red<P>(w.x, w.y, ov.cw);
           }
-          dif_rt<P, RS0, SLO0, 1>(v, twf + o);
+          dif_rt<P, RS0, SLO0, 1, true>(v, s_tw + o);
         }
       } else if (half) {
         const int g0 = (o << lgC) + col;
@@ -902,11 +903,17 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
   const bool half = ov.kc <= (job.L >> 1);
   const int rows = half ? (1 << (LGR - 1)) : (1 << LGR);
   uint2* stage = reinterpret_cast<uint2*>(smem + sm_len(LGR) * CT);
-  stage_operand(ov, stage, rows, lct, LGC, tile << lct);
+  // the first pass's stage twiddles (entries < 2^(SLO0 + RS0)) of every prime
+  constexpr PassPlan PP = pass_plan(LGR);
+  constexpr int NTW = 1 << (PP.slo[0] + PP.rs[0]);
+  uint2* s_tw = stage + (rows << lct);
+  for (int i = threadIdx.x; i < job.np * NTW; i += blockDim.x)
+    s_tw[i] = __ldg(tab.stw + ((i / NTW) * 2) * kTwN + (i % NTW));
+  stage_operand(ov, stage, rows, lct, LGC, tile << lct);  // (its barrier covers s_tw too)
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
     if (P < job.np) {
-      col_fwd_body<P, LGR, LGC, true>(job, tab, lct, b, op, tile, stage);
+      col_fwd_body<P, LGR, LGC, true>(job, tab, lct, b, op, tile, stage, s_tw + P * NTW);
       __syncthreads();  // the next prime reuses the transform panel
     }
   });

@@ -186,7 +186,8 @@ __device__ __forceinline__ void dit_ct(u32 (&v)[1 << RS]) {
 }
 
 // DIF over stages SLO+RS-1 .. SLO with table twiddles; two = tw + o.
-template <int P, int RS, int SLO, int NV>
+// (SMEM: `two` points into shared memory -- plain loads instead of __ldg)
+template <int P, int RS, int SLO, int NV, bool SMEM = false>
 __device__ __forceinline__ void dif_rt(u32 (&v)[NV][1 << RS], const uint2* __restrict__ two) {
   sfor<RS>([&](auto st_) {
     constexpr int st = decltype(st_)::value;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void dif_rt(u32 (&v)[NV][1 << RS], const uint2* __res
       constexpr int k = decltype(k_)::value;
       if constexpr ((k & hr) == 0) {
         constexpr int off = (1 << (sg + SLO)) + ((k & (hr - 1)) << SLO);
-        const uint2 w = __ldg(two + off);
+        const uint2 w = SMEM ? two[off] : __ldg(two + off);
 #pragma unroll
         for (int j = 0; j < NV; ++j) bf_dif<P>(v[j][k], v[j][k + hr], w.x, w.y);
       }
@@ -206,13 +207,13 @@ __device__ __forceinline__ void dif_rt(u32 (&v)[NV][1 << RS], const uint2* __res
 
 // As dif_rt, but the upper half of the inputs (k >= 2^(RS-1)) is known to be
 // zero (zero-padded operand): the first stage is y = x * w, x unchanged.
-template <int P, int RS, int SLO>
+template <int P, int RS, int SLO, bool SMEM = false>
 __device__ __forceinline__ void dif_rt_half(u32 (&v)[1][1 << RS], const uint2* __restrict__ two) {
   constexpr int H = 1 << (RS - 1);
   sfor<H>([&](auto k_) {
     constexpr int k = decltype(k_)::value;
     constexpr int off = (1 << (RS - 1 + SLO)) + (k << SLO);
-    const uint2 w = __ldg(two + off);
+    const uint2 w = SMEM ? two[off] : __ldg(two + off);
     v[0][k + H] = v[0][k] * w.x - __umulhi(v[0][k], w.y) * PK<P>::p;
   });
   sfor<RS - 1>([&](auto st_) {
@@ -223,7 +224,7 @@ __device__ __forceinline__ void dif_rt_half(u32 (&v)[1][1 << RS], const uint2* _
       constexpr int k = decltype(k_)::value;
       if constexpr ((k & hr) == 0) {
         constexpr int off = (1 << (sg + SLO)) + ((k & (hr - 1)) << SLO);
-        const uint2 w = __ldg(two + off);
+        const uint2 w = SMEM ? two[off] : __ldg(two + off);
         bf_dif<P>(v[0][k], v[0][k + hr], w.x, w.y);
       }
     });

@@ -889,7 +889,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const unsigned ctas_all = (1u << (job.lgC - lct)) * 2u * (unsigned)job.batch;
   if (job.m == 1 && fwd_all) {
     const int rows = kcmax <= (job.L >> 1) ? (int)(R >> 1) : (int)R;
-    const size_t sma = smc + (size_t)rows * (1u << lct) * 8;
+    const PassPlan pp = pass_plan(job.lgR);
+    const size_t ntw = (size_t)job.np << (pp.slo[0] + pp.rs[0]);  // staged first-pass twiddles
+    const size_t sma = smc + (size_t)rows * (1u << lct) * 8 + ntw * 8;
     prof::Scope ps_("k_col_fwd", st);
     col_fwd_all_kernel(job.lgR, job.lgC)<<<ctas_all, threads, sma, st>>>(job, tab, lct);
   } else if (job.m > 1 && fwd_all) {
