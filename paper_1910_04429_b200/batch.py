@@ -74,9 +74,10 @@ class HashEngine:
         if out is None:
             out = torch.empty((b, self.rbytes), dtype=torch.uint8, device=self.device)
         ws = self._workspace(st)
-        _native.check(self.lib.pab_hash_batch(
-            _ptr(x), _ptr(c), _ptr(d), x.stride(0), self.n, self.r, b, self.order,
-            _ptr(out), out.stride(0), _ptr(ws), self.ws_bytes, ctypes.c_void_p(st.cuda_stream)))
+        with torch.cuda.device(self.device):  # the C ABI works on the current device
+            _native.check(self.lib.pab_hash_batch(
+                _ptr(x), _ptr(c), _ptr(d), x.stride(0), self.n, self.r, b, self.order,
+                _ptr(out), out.stride(0), _ptr(ws), self.ws_bytes, ctypes.c_void_p(st.cuda_stream)))
         return out
 
     def hash_host(self, x: torch.Tensor, c: torch.Tensor, d: torch.Tensor,
