@@ -927,7 +927,13 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   }
   {
     prof::Scope ps_("k_col_inv", st);
-    ci<<<dim3(1u << (job.lgC - lct), job.batch, job.np), ct_threads, smc, st>>>(job, tab, lct);
+    // pow2 inverse: half-width tiles in 128-thread CTAs while >= 32 columns wide
+    // (same resident warps, more independent CTAs; measured -1.5%)
+    const int xi = job.m == 1 && lct >= 6 ? 1 : 0;
+    const int lci = lct - xi;
+    const size_t smi = (size_t)job.m * sm_len(job.lgR) * (1u << lci) * 4;
+    ci<<<dim3(1u << (job.lgC - lci), job.batch, job.np), ct_threads >> xi, smi, st>>>(job, tab,
+                                                                                   lci);
   }
 }
 
