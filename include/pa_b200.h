@@ -103,6 +103,31 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
                   uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device);
 
 /*
+ * Seed expansion on the device (SHAKE-256): for j < batch, the hash-family
+ * member of block i = first_index + j exactly as run_pa derives it,
+ *   gen_seed(n, derive_block_seed(master, i))          pkg/src/modpa/pa.py:156-172
+ * with _expand (pa.py:138-153) as the XOF; run_pa's call site is
+ * pkg/src/modpa/bench.py:258.  master = the seed material bytes (an int seed s
+ * is s.to_bytes(max(1, ceil(bitlen/8)), "little"), pa.py:142-144), at most 1024
+ * bytes, host memory.  c and d (device) receive ceil(n/8) bytes per block at
+ * offset j*stride in byte_order (c with its low bit set, bits >= n cleared),
+ * ready for pab_hash_batch.  Asynchronous on `stream`.
+ */
+int pab_seed_expand(const uint8_t* master, uint64_t master_len, uint64_t first_index,
+                    uint32_t batch, uint64_t n_bits, int byte_order, uint8_t* c, uint8_t* d,
+                    uint64_t stride, void* stream);
+
+/*
+ * Host-buffer run_pa step on `device` (pkg/src/modpa/bench.py:256-262 for a
+ * contiguous run of blocks): x = batch*ceil(n/8) host bytes (blocks first_index
+ * .. first_index+batch-1 of the key file), seeds derived on the device by
+ * pab_seed_expand, out = batch*ceil(r/8) host bytes.  Blocks until done.
+ */
+int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
+                         int byte_order, const uint8_t* master, uint64_t master_len,
+                         uint64_t first_index, uint8_t* out, int device);
+
+/*
  * Exact product of two naturals given as LSF byte strings (bignum.mul,
  * pkg/src/modpa/bignum.py:194-231): out receives a_bytes + b_bytes LSF bytes.
  */

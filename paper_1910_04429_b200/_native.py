@@ -40,6 +40,12 @@ SIGNATURES = {
                                       ctypes.c_uint64, _u8p, ctypes.c_size_t, _u8p]),
     "pab_hash_host": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_int]),
+    "pab_seed_expand": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                       ctypes.c_uint64, ctypes.c_int, _u8p, _u8p,
+                                       ctypes.c_uint64, _u8p]),
+    "pab_hash_seeded_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_uint64,
+                                            ctypes.c_uint64, _u8p, ctypes.c_int]),
     "pab_mul_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint64]),
     "pab_mul": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p, _u8p,
                                ctypes.c_size_t, _u8p]),
@@ -103,6 +109,30 @@ def hash_host(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
     dev = _device() if device is None else device
     out = ctypes.create_string_buffer(batch * ((r + 7) // 8))
     check(lib.pab_hash_host(x, c, d, n, r, batch, order, out, dev))
+    return out.raw
+
+
+MAX_SEED_MATERIAL = 1024  # bytes of master seed material the device expander takes
+
+
+def seed_material(rng_seed) -> bytes:
+    """Seed material bytes exactly as _expand reads them (pkg/src/modpa/pa.py:141-146)."""
+    if isinstance(rng_seed, int):
+        if rng_seed < 0:
+            raise ValueError("integer seed material must be nonnegative")
+        return rng_seed.to_bytes(max(1, (rng_seed.bit_length() + 7) // 8), "little")
+    return bytes(rng_seed)
+
+
+def hash_seeded_host(x: bytes, n: int, r: int, batch: int, rng_seed, first_index: int = 0,
+                     order: int = ORDER_LSF, device: int | None = None) -> bytes:
+    """run_pa's per-block step for `batch` contiguous blocks: x from the host, each block's
+    (c, d) = gen_seed(n, derive_block_seed(rng_seed, first_index + j)) derived on the GPU."""
+    lib = load()
+    dev = _device() if device is None else device
+    m = seed_material(rng_seed)
+    out = ctypes.create_string_buffer(batch * ((r + 7) // 8))
+    check(lib.pab_hash_seeded_host(x, n, r, batch, order, m, len(m), first_index, out, dev))
     return out.raw
 
 

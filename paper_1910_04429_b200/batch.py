@@ -125,6 +125,94 @@ class HashEngine:
             cur.wait_stream(s)
         return out
 
+    def seed_device(self, rng_seed, first_index: int, batch: int, c: torch.Tensor,
+                    d: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
+        """(c, d) of blocks first_index .. first_index+batch-1 as run_pa derives them,
+        gen_seed(n, derive_block_seed(rng_seed, i)) (pkg/src/modpa/pa.py:138-172),
+        SHAKE-256 on the device into rows of c and d (asynchronous on `stream`)."""
+        for t in (c, d):
+            if t.device != self.device or t.dtype != torch.uint8 or t.dim() != 2:
+                raise ValueError("c, d must be 2-D uint8 tensors on the engine's device")
+            if t.shape[0] < batch or t.shape[1] < self.nbytes or t.stride(1) != 1:
+                raise ValueError("c, d must be [>= batch, >= ceil(n/8)] with unit byte stride")
+        if c.stride(0) != d.stride(0):
+            raise ValueError("c and d must share one row stride")
+        m = _native.seed_material(rng_seed)
+        st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.pab_seed_expand(
+                m, len(m), first_index, batch, self.n, self.order, _ptr(c), _ptr(d), c.stride(0),
+                ctypes.c_void_p(st.cuda_stream)))
+
+    def hash_seeded_host(self, x: torch.Tensor, rng_seed, first_index: int = 0,
+                         out: torch.Tensor | None = None, streams: int = 3,
+                         chunk: int | None = None) -> torch.Tensor:
+        """run_pa's step end to end: key blocks x from (pinned) host memory, block
+        first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
+        derived on the GPU (only x crosses PCIe).
+
+        The seed expansion is latency-bound per XOF stream (a chain of dependent
+        Keccak-f calls), so the whole call's seeds are expanded by one launch on a
+        stream of their own, into one of two alternating buffers: the next call's
+        expansion runs beside this call's hashing.  H2D of x, hashing and D2H are
+        pipelined over `streams` slots as in hash_host.
+        """
+        b = x.shape[0]
+        if out is None:
+            out = torch.empty((b, self.rbytes), dtype=torch.uint8, pin_memory=True)
+        chunk = chunk or self.chunk
+        nslots = max(1, streams)
+        s_in, s_comp, s_out = self._pipe_streams()
+        s_seed = self._seed_stream()
+        bufs = self._io_buffers(nslots, chunk)
+        ev = self._slot_events(nslots)
+        sc, sd, ev_free, ev_ready = self._seed_buffers(b)
+        cur = torch.cuda.current_stream(self.device)
+        for s in (s_in, s_comp, s_out, s_seed):
+            s.wait_stream(cur)
+        s_seed.wait_event(ev_free)               # the previous user of this buffer is done
+        self.seed_device(rng_seed, first_index, b, sc, sd, stream=s_seed)
+        ev_ready.record(s_seed)
+        s_comp.wait_event(ev_ready)
+        for i, b0 in enumerate(range(0, b, chunk)):
+            k = i % nslots
+            dx, _, _, dout = bufs[k]
+            nb = min(chunk, b - b0)
+            s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
+            with torch.cuda.stream(s_in):
+                dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
+                ev["in"][k].record(s_in)
+            s_comp.wait_event(ev["in"][k])
+            s_comp.wait_event(ev["out"][k])      # slot k's output drained
+            self.hash_device(dx[:nb], sc[b0:b0 + nb], sd[b0:b0 + nb], dout[:nb], stream=s_comp)
+            ev["comp"][k].record(s_comp)
+            s_out.wait_event(ev["comp"][k])
+            with torch.cuda.stream(s_out):
+                out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
+                ev["out"][k].record(s_out)
+        ev_free.record(s_comp)
+        for s in (s_in, s_comp, s_out, s_seed):
+            cur.wait_stream(s)
+        return out
+
+    def _seed_buffers(self, b: int):
+        """Two alternating [b, ceil(n/8)] (c, d) buffers with their free / ready events."""
+        if getattr(self, "_sb_rows", 0) < b:
+            if getattr(self, "_sb_rows", 0):
+                torch.cuda.synchronize(self.device)  # old buffers may still be in use
+            mk = lambda: torch.empty((b, self.nbytes), dtype=torch.uint8, device=self.device)  # noqa: E731
+            self._sb = [(mk(), mk(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
+            self._sb_rows = b
+            self._sb_next = 0
+        c, d, free, ready = self._sb[self._sb_next]
+        self._sb_next ^= 1
+        return c[:b], d[:b], free, ready
+
+    def _seed_stream(self):
+        if not hasattr(self, "_sseed"):
+            self._sseed = torch.cuda.Stream(self.device)
+        return self._sseed
+
     def _pipe_streams(self):
         if not hasattr(self, "_pipe"):
             self._pipe = tuple(torch.cuda.Stream(self.device) for _ in range(3))
@@ -133,7 +221,7 @@ class HashEngine:
     def _slot_events(self, k: int):
         if getattr(self, "_ev_k", None) != k:
             mk = lambda: [torch.cuda.Event() for _ in range(k)]  # noqa: E731
-            self._ev = {"in": mk(), "comp": mk(), "out": mk()}
+            self._ev = {"in": mk(), "comp": mk(), "out": mk(), "seed": mk()}
             self._ev_k = k
         return self._ev
 
@@ -147,17 +235,20 @@ class HashEngine:
         return self._io
 
 
-def hash_host_multi(x: torch.Tensor, c: torch.Tensor, d: torch.Tensor, n: int, r: int, *,
-                    devices: list[int] | None = None, order: int = _native.ORDER_LSF,
-                    max_batch: int = 256) -> torch.Tensor:
+def hash_host_multi(x: torch.Tensor, c: torch.Tensor | None, d: torch.Tensor | None, n: int,
+                    r: int, *, devices: list[int] | None = None, order: int = _native.ORDER_LSF,
+                    max_batch: int = 256, rng_seed=None, first_index: int = 0) -> torch.Tensor:
     """Hash a pinned host batch on several GPUs of this process: one worker thread per
     device, contiguous block shards, keys returned in block order.
 
     Blocks are independent (SURVEY.md §8e), so there is no inter-GPU traffic;
     each worker runs HashEngine.hash_host on its shard (copies overlapped with
     compute on that device's streams).  The C ABI releases the GIL, so the
-    workers run concurrently.
+    workers run concurrently.  With c = d = None the seeds are derived on the
+    GPUs from `rng_seed` (block i of x is run_pa block first_index + i).
     """
+    if (c is None) != (d is None) or (c is None and rng_seed is None):
+        raise ValueError("give both c and d, or neither and an rng_seed")
     import threading
 
     devs = list(range(torch.cuda.device_count())) if devices is None else list(devices)
@@ -180,7 +271,10 @@ def hash_host_multi(x: torch.Tensor, c: torch.Tensor, d: torch.Tensor, n: int, r
                 return
             torch.cuda.set_device(dev)
             eng = HashEngine(n, r, device=dev, order=order, max_batch=min(max_batch, hi - lo))
-            eng.hash_host(x[lo:hi], c[lo:hi], d[lo:hi], out[lo:hi], streams=3)
+            if c is None:
+                eng.hash_seeded_host(x[lo:hi], rng_seed, first_index + lo, out[lo:hi], streams=3)
+            else:
+                eng.hash_host(x[lo:hi], c[lo:hi], d[lo:hi], out[lo:hi], streams=3)
             torch.cuda.synchronize(dev)
         except BaseException as e:  # surfaced in the caller
             errors.append(e)

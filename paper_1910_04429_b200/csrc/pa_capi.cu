@@ -683,6 +683,74 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
   return PAB_OK;
 }
 
+int pab_seed_expand(const uint8_t* master, uint64_t master_len, uint64_t first_index,
+                    uint32_t batch, uint64_t n_bits, int byte_order, uint8_t* c, uint8_t* d,
+                    uint64_t stride, void* stream) {
+  if (n_bits < 1) return fail(PAB_EINVAL, "alpha must be >= 1, got 0");
+  if (n_bits > ((u64)1 << 40)) return fail(PAB_ERANGE, "block size beyond the seed expander");
+  if (master_len > (u64)kMaxSeedMaster)
+    return fail(PAB_EINVAL, "seed material longer than " + std::to_string(kMaxSeedMaster) +
+                                " bytes");
+  if (master_len && !master) return fail(PAB_EINVAL, "null seed material");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  if (batch == 0) return PAB_OK;
+  if (!c || !d) return fail(PAB_EINVAL, "null pointer argument");
+  const u64 nbytes = ceil_div(n_bits, 8);
+  if (stride < nbytes) return fail(PAB_EINVAL, "stride smaller than the block byte length");
+  if (first_index > ~0ull - batch) return fail(PAB_EINVAL, "block index overflows 64 bits");
+  SeedMaster sm;
+  std::memset(&sm, 0, sizeof(sm));
+  if (master_len) std::memcpy(sm.b, master, master_len);
+  const int msf = byte_order == PAB_ORDER_MSF;
+  const int word_io = !msf && stride % 8 == 0 && aligned(c, 8) && aligned(d, 8);
+  launch_seed_expand(sm, (int)master_len, (unsigned long long)first_index, (int)batch,
+                     (long long)n_bits, msf, word_io, c, d, (long long)stride,
+                     (cudaStream_t)stream);
+  CK(cudaGetLastError(), "kernel launch");
+  return PAB_OK;
+}
+
+int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
+                         int byte_order, const uint8_t* master, uint64_t master_len,
+                         uint64_t first_index, uint8_t* out, int device) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, r_bits, &g);
+  if (rc) return rc;
+  if (batch == 0) return PAB_OK;
+  if (!x || !out) return fail(PAB_EINVAL, "null pointer argument");
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  DevState* ds;
+  if ((rc = ensure_device(device, &ds))) return rc;
+  HostCtx& h = ds->host;
+  std::lock_guard<std::mutex> lk(h.mu);
+  const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
+  const u64 in_stride = round_up(nbytes, 16), out_stride = round_up(rbytes, 16);
+  u64 chunk = batch;
+  while (chunk > 1 && pab_hash_workspace_bytes(n_bits, (uint32_t)chunk) > ((size_t)2 << 30))
+    chunk /= 2;
+  const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, (uint32_t)chunk);
+  const size_t io_bytes = (size_t)batch * (3 * in_stride + out_stride);
+  if ((rc = host_ensure(h, ws_bytes, io_bytes))) return rc;
+  uint8_t* dx = h.dev_io;
+  uint8_t* dc = dx + batch * in_stride;
+  uint8_t* dd = dc + batch * in_stride;
+  uint8_t* dout = dd + batch * in_stride;
+  if ((rc = pab_seed_expand(master, master_len, first_index, batch, n_bits, byte_order, dc, dd,
+                            in_stride, h.stream)))
+    return rc;
+  CK(cudaMemcpy2DAsync(dx, in_stride, x, nbytes, nbytes, batch, cudaMemcpyHostToDevice, h.stream),
+     "H2D x");
+  rc = pab_hash_batch(dx, dc, dd, in_stride, n_bits, r_bits, batch, byte_order, dout, out_stride,
+                      h.ws, h.ws_bytes, h.stream);
+  if (rc) return rc;
+  CK(cudaMemcpy2DAsync(out, rbytes, dout, out_stride, rbytes, batch, cudaMemcpyDeviceToHost,
+                       h.stream),
+     "D2H out");
+  CK(cudaStreamSynchronize(h.stream), "synchronize");
+  return PAB_OK;
+}
+
 size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes) {
   const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4);
   if (ka == 0 || kb == 0) return 256;

@@ -77,6 +77,19 @@ void launch_unpack(const u32* words, long long word_stride, long long m_bits, in
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st);
 // CRT + carry + mask + shift -> output.
 void launch_carry(const ConvJob& job, cudaStream_t st);
+// gen_seed(n, derive_block_seed(master, first + j)) for j < batch on the GPU
+// (SHAKE-256, pkg/src/modpa/pa.py:138-172): c and d rows at j * stride bytes,
+// ceil(n/8) bytes each in byte order msf; word_io = LSF rows 8-byte aligned.
+constexpr int kMaxSeedMaster = 1024;  // master seed material bytes (kernel parameter)
+struct SeedMaster {
+  uint8_t b[kMaxSeedMaster];
+};
+void launch_seed_expand(const SeedMaster& master, int mlen, unsigned long long first, int batch,
+                        long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
+                        long long stride, cudaStream_t st);
+void seed_expand_raw(const SeedMaster& master, int mlen, unsigned long long first, int batch,
+                     long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
+                     long long stride, cudaStream_t st);
 // a kernel set exists for this geometry (L = m * 2^(lgR + lgC))
 bool conv_supported(int m, int lgR, int lgC);
 

@@ -115,6 +115,32 @@ def gpu_hasher(batch: int = 256, devices: list[int] | None = None) -> Hasher:
     return run
 
 
+# seeded(x, n, r, order, rng_seed, first_index) -> [B, ceil(r/8)] uint8: block j of x is
+# run_pa block first_index + j; its seed is derived by the implementation itself
+SeededHasher = Callable[[np.ndarray, int, int, WordOrder, int, int], np.ndarray]
+
+
+def gpu_seeded_hasher(batch: int = 256, devices: list[int] | None = None) -> SeededHasher:
+    """Default run_pa path: only the key blocks go to the GPU; each block's
+    gen_seed(n, derive_block_seed(rng_seed, i)) is expanded there (SHAKE-256,
+    pab_seed_expand), beside the hashing of the previous chunk."""
+
+    def run(x, n, r, order, rng_seed, first_index):
+        import torch
+
+        from .batch import hash_host_multi
+
+        devs = devices if devices is not None else [torch.cuda.current_device()]
+        px = torch.from_numpy(np.array(x, copy=True)).pin_memory()
+        out = hash_host_multi(px, None, None, n, r, devices=devs, max_batch=batch,
+                              rng_seed=rng_seed, first_index=first_index,
+                              order=_native.ORDER_MSF if order is WordOrder.MOST_SIGNIFICANT_FIRST
+                              else _native.ORDER_LSF)
+        return out.numpy()
+
+    return run
+
+
 def derive_seeds(n: int, rng_seed: int, indices, order: WordOrder,
                  threads: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     """(c, d) of the given block indices, serialized in `order` (pa.py:156-172)."""
@@ -142,12 +168,14 @@ def shard_range(nblocks: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
-           chunk_blocks: int = 1024) -> PaRunResult:
+           chunk_blocks: int = 1024, seeded: SeededHasher | None = None) -> PaRunResult:
     """Hash every complete n-bit block of cfg.in_path into r bits (bench.py:223-265).
 
     `dist` is torch.distributed (initialised) for multi-GPU runs; each rank
-    hashes its contiguous share and rank 0 writes the file.  `hasher` defaults
-    to the GPU path; tests may inject another implementation.
+    hashes its contiguous share and rank 0 writes the file.  By default the
+    GPU derives the seeds and hashes (`gpu_seeded_hasher`); an injected
+    `hasher` gets host-derived (c, d) instead (tests use the oracle), an
+    injected `seeded` replaces the default seeded path.
     """
     if len(cfg.sizes) != 1:
         raise ValueError("batch hashing needs exactly one block size")
@@ -179,7 +207,8 @@ def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
         budget = {"h_min": cfg.h_min, "epsilon": cfg.epsilon, "r": r,
                   "eps_bar_log2": security.leftover_bound_log2(cfg.h_min, r, cfg.epsilon)}
 
-    hasher = hasher or gpu_hasher()
+    if hasher is None and seeded is None:
+        seeded = gpu_seeded_hasher()
     lo, hi = shard_range(nblocks, rank, world)
     arr = np.frombuffer(data, np.uint8, count=nblocks * block_bytes).reshape(nblocks, block_bytes)
     rb = (r + 7) // 8
@@ -188,8 +217,12 @@ def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
         b1 = min(hi, b0 + chunk_blocks)
         x = arr[b0:b1]
         # import_block's check: no bits beyond n (n % 8 == 0 here, so none exist)
-        c, d = derive_seeds(n, cfg.rng_seed, range(b0, b1), cfg.order)
-        parts.append(np.asarray(hasher(x, c, d, n, r, cfg.order), np.uint8).reshape(b1 - b0, rb))
+        if seeded is not None:
+            y = seeded(x, n, r, cfg.order, cfg.rng_seed, b0)
+        else:
+            c, d = derive_seeds(n, cfg.rng_seed, range(b0, b1), cfg.order)
+            y = hasher(x, c, d, n, r, cfg.order)
+        parts.append(np.asarray(y, np.uint8).reshape(b1 - b0, rb))
     mine = np.concatenate(parts) if parts else np.empty((0, rb), np.uint8)
 
     if dist and world > 1:

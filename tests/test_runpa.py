@@ -131,7 +131,18 @@ def test_run_pa_gloo_world2_matches_reference(tmp_path, which):
 
 @pytest.mark.gpu
 def test_run_pa_gpu_matches_reference_files(tmp_path):
+    # default path: key blocks to the GPU, seeds expanded there (pab_seed_expand)
     for i, case in enumerate(load_cases()):
         cfg, out = _cfg(case, tmp_path, str(i))
         run_pa(cfg)
+        assert out.read_bytes().hex() == case["out"], case["n"]
+
+
+@pytest.mark.gpu
+def test_run_pa_gpu_host_seeds_matches_reference_files(tmp_path):
+    from paper_1910_04429_b200.runpa import gpu_hasher
+
+    for i, case in enumerate(load_cases()):
+        cfg, out = _cfg(case, tmp_path, "h" + str(i))
+        run_pa(cfg, hasher=gpu_hasher(), chunk_blocks=3)
         assert out.read_bytes().hex() == case["out"], case["n"]
