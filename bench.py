@@ -12,6 +12,8 @@ scaling (blocks shard by index, no collective on the data path).
 `value`  : device-resident Mbps (inputs already in HBM), max-over-ranks time.
 `e2e`    : same metric through the public batched API from pinned host memory,
            H2D of x, c, d and D2H of the keys inside the timed region.
+`e2e_run_pa`: run_pa's scope (n <= 1e7): only the key blocks x cross PCIe; each
+           block's (c, d) is expanded on the GPU (SHAKE-256) beside the hashing.
 `--impl reference`: the reference's CPU algorithm (the C port under oracle/,
            all host threads, rank 0 only) on a bounded sample of the workload.
 """
@@ -346,10 +348,56 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
            "h2d_gbps": round(3 * per_rank * eng.nbytes / (e2e_ms * 1e-3) / 1e9, 1),
            "frac_of_copy_bound": round(copy_ms / e2e_ms, 4)}
 
+    e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) \
+        if n <= 10_000_000 else None
+
     res = {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
+           "e2e_seeded": e2e_seeded,
            "out": first_out, "per_rank": per_rank, "n": n, "r": r, "eng": eng,
            "dist": dist, "seeds": seeds}
     return res
+
+
+def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) -> dict:
+    """run_pa's scope end to end (pkg/src/modpa/bench.py:256-262): the key blocks
+    from pinned host memory, block i hashed with gen_seed(n, derive_block_seed(0, i))
+    expanded on the GPU (HashEngine.hash_seeded_host), keys back to the host.  Only
+    x crosses PCIe.  Rank k hashes run_pa blocks k*B .. k*B+B-1."""
+    import torch
+    from paper_1910_04429_b200 import pa
+
+    first = rank * per_rank
+    hout = torch.empty((per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
+    for _ in range(max(1, args.warmup)):
+        eng.hash_seeded_host(px, 0, first, hout, streams=3)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        eng.hash_seeded_host(px, 0, first, hout, streams=3)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist)
+    # spot check: two blocks against host-derived seeds through the device path
+    nb = eng.nbytes
+    idx = [0, per_rank - 1]
+    dx = px[idx].cuda()
+    dc = torch.empty((2, nb), dtype=torch.uint8)
+    dd = torch.empty_like(dc)
+    for j, i in enumerate(idx):
+        sd = pa.gen_seed(n, pa.derive_block_seed(0, first + i))
+        dc[j] = torch.frombuffer(bytearray(sd.c.value.to_bytes(nb, "little")), dtype=torch.uint8)
+        dd[j] = torch.frombuffer(bytearray(sd.d.value.to_bytes(nb, "little")), dtype=torch.uint8)
+    want = eng.hash_device(dx, dc.cuda(), dd.cuda()).cpu()
+    assert torch.equal(hout[idx], want), "run_pa e2e keys differ from host-derived seeds"
+    return {"value": round(bits_step / (ms * 1e-3) / 1e6, 1), "unit": "Mbps",
+            "scope": "run_pa: x pinned host -> GPU, (c, d) = gen_seed(n, derive_block_seed(0, i))"
+                     " expanded on the GPU (SHAKE-256), keys -> host",
+            "h2d_bytes_per_step": per_rank * nb, "d2h_bytes_per_step": per_rank * eng.rbytes,
+            "ms_per_step": round(ms, 4)}
 
 
 def ncu_traffic(workload: str | None, batch: int | None = None) -> dict:
@@ -552,7 +600,8 @@ def main():
                        "parallelism": f"blocks sharded by index over {world} GPU(s), no collective",
                        "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
                              % (3 * per_rank * ((n + 7) // 8) / 1e6)},
-            "e2e": res["e2e"], "gpu_launches": launches, "roofline": roof,
+            "e2e": res["e2e"], "e2e_run_pa": res["e2e_seeded"], "gpu_launches": launches,
+            "roofline": roof,
             "step_roofline": step_roof, "baseline_roofline": base_roof, "dropin": dropin,
             "kernels": kernels, "clocks": res["clocks"], "cpu_baseline": cpu,
         }

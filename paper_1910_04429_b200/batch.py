@@ -168,9 +168,11 @@ class HashEngine:
         ev = self._slot_events(nslots)
         sc, sd, ev_free, ev_ready = self._seed_buffers(b)
         cur = torch.cuda.current_stream(self.device)
-        for s in (s_in, s_comp, s_out, s_seed):
+        for s in (s_in, s_comp, s_out):
             s.wait_stream(cur)
-        s_seed.wait_event(ev_free)               # the previous user of this buffer is done
+        # the expansion reads nothing of the caller's: it only waits for its buffer
+        # (so it runs ahead, beside the previous call's hashing)
+        s_seed.wait_event(ev_free)
         self.seed_device(rng_seed, first_index, b, sc, sd, stream=s_seed)
         ev_ready.record(s_seed)
         s_comp.wait_event(ev_ready)
@@ -191,7 +193,7 @@ class HashEngine:
                 out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
                 ev["out"][k].record(s_out)
         ev_free.record(s_comp)
-        for s in (s_in, s_comp, s_out, s_seed):
+        for s in (s_in, s_comp, s_out):        # s_comp has waited for s_seed's launch
             cur.wait_stream(s)
         return out
 
