@@ -272,8 +272,9 @@ __device__ __forceinline__ u32 fetch_word(const u32* __restrict__ src, long long
 
 struct CarrySmem {
   u32 tile, cin;
+  volatile u32 cin_ready;  // look-back mode: sm.cin valid (set by warp 0)
   u32 wq[kCarryWarps], wt[kCarryWarps];
-  u32 first[kCarryWarps];
+  u32 first[kCarryWarps];  // each warp's first word, resolved with carry-in 0
   // cw = 2: high words of each warp's top two coefficients for the warp above
   // (w2, w3 of lane 31, w4 of lanes 30 and 31), double-buffered by tile parity
   u32 nb[2][kCarryWarps][4];
@@ -527,6 +528,8 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
   if (lane == 0) {
     sm.wq[warp] = f.q;
     sm.wt[warp] = f.t;
+    sm.first[warp] = T[0];
+    if (LOOKBACK && warp == 0) sm.cin_ready = 0u;
   }
   __syncthreads();
   CarryFn wpre{0, 0, true}, agg{0, 0, true};
@@ -536,7 +539,10 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
     if (w < warp) wpre = cf_compose(fw, wpre);
     agg = cf_compose(fw, agg);
   }
-  // carry into the tile
+  // carry into the tile.  Only warp 0, and a warp whose predecessors in the tile
+  // let a carry through (wpre.t != kInf: all-ones runs, rare), depend on it; the
+  // others go on without waiting for the look-back (ncu: 26% barrier stalls).
+  u32 tile_cin = cin_seq;
   if (LOOKBACK) {
     if (warp == 0) {  // decoupled look-back: 32 predecessor tiles per probe
       volatile unsigned long long* st = job.tile_state + (long long)b * job.tiles;
@@ -569,13 +575,17 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
       if (lane == 0) {
         st[tile] = (2ull << 62) | ((unsigned long long)cf_apply(agg, cin) << 32);
         sm.cin = cin;
+        __threadfence_block();
+        sm.cin_ready = 1u;
       }
+      tile_cin = cin;
+    } else if (wpre.t != kInf) {
+      while (sm.cin_ready == 0u) {
+      }
+      __threadfence_block();
+      tile_cin = *((volatile u32*)&sm.cin);
     }
-  } else if (threadIdx.x == 0) {
-    sm.cin = cin_seq;
   }
-  __syncthreads();
-  const u32 tile_cin = sm.cin;
 
   // add the real carry-in at word 0 and ripple it through all-ones words
   // (almost always it stops in word 0)
@@ -607,19 +617,20 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
       T[i] = w >= nT ? 0u : (w == nT - 1 ? (T[i] & tmask) : T[i]);
     }
   }
-  // word after this warp's last word: next warp's first word, or (last warp)
-  // the next tile's first word = S_next + carry
-  if (lane == 0) sm.first[warp] = T[0];
-  u32 nextw = 0;
-  if (last) {
-    const long long k = wb + NR * 32;  // first word of the next tile
-    const u32 dv = fetch_word(dw, k, kd, job.maskD);
-    const u64 sn = s_next + dv + c;
-    nextw = (u32)sn;
+  // word after this warp's last word: the next warp's first word resolved with
+  // carry-in 0, plus this warp's carry out; or (last warp) the next tile's first
+  // word = S_next + carry
+  u32 nextw;
+  {
+    const long long k = wb + NR * 32;  // first word after the warp
+    if (last) {
+      const u32 dv = fetch_word(dw, k, kd, job.maskD);
+      nextw = (u32)(s_next + dv + c);
+    } else {
+      nextw = sm.first[warp + 1] + c;
+    }
     nextw = k >= nT ? 0u : (k == nT - 1 ? (nextw & tmask) : nextw);
   }
-  __syncthreads();
-  if (warp < kCarryWarps - 1) nextw = sm.first[warp + 1];
   // output words y_o = (T >> shift), o = w - shift/32
   const long long ws = job.shift >> 5;
   const int sh = (int)(job.shift & 31);
