@@ -313,8 +313,10 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for _ in range(args.steps):
-        eng.hash_host(px, pc, pd, hout, streams=3, chunk=cfg.get("e2e_chunk"))
+    for i in range(args.steps):  # streamed: each step's head overlaps the previous tail
+        eng.hash_host(px, pc, pd, hout, streams=3, chunk=cfg.get("e2e_chunk"),
+                      join_in=i == 0, join_out=False)
+    eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
     clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
@@ -376,8 +378,9 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) -> dict:
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for _ in range(args.steps):
-        eng.hash_seeded_host(px, 0, first, hout, streams=3)
+    for i in range(args.steps):
+        eng.hash_seeded_host(px, 0, first, hout, streams=3, join_in=i == 0, join_out=False)
+    eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist)

@@ -82,15 +82,22 @@ class HashEngine:
 
     def hash_host(self, x: torch.Tensor, c: torch.Tensor, d: torch.Tensor,
                   out: torch.Tensor | None = None, streams: int = 3,
-                  chunk: int | None = None) -> torch.Tensor:
+                  chunk: int | None = None, join_in: bool = True,
+                  join_out: bool = True) -> torch.Tensor:
         """End-to-end from (pinned) host tensors: H2D, hash, D2H, overlapped.
 
         A triple-buffered pipeline: one stream each for H2D, hashing and D2H,
         `streams` device buffer slots, and per-slot events so the copy engines
         only wait for a slot to be free (the H2D of chunk i+slots waits for the
         hashing of chunk i to have read its inputs).  The slot events persist
-        across calls, so back-to-back calls overlap as well.  Returns host
-        [batch, ceil(r/8)] (complete once the caller's current stream is synced).
+        across calls.  Returns host [batch, ceil(r/8)] (complete once the
+        caller's current stream is synced).
+
+        Streaming use: join_in=False skips ordering the copies after the
+        caller's stream (the inputs are ready host memory), join_out=False skips
+        making the caller's stream wait for the keys; consecutive calls then
+        overlap (one call's head with the previous call's tail) and the caller
+        calls join() once before reading the keys.
         """
         b = x.shape[0]
         if out is None:
@@ -101,8 +108,9 @@ class HashEngine:
         bufs = self._io_buffers(nslots, chunk)
         ev = self._slot_events(nslots)
         cur = torch.cuda.current_stream(self.device)
-        for s in (s_in, s_comp, s_out):
-            s.wait_stream(cur)
+        if join_in:
+            for s in (s_in, s_comp, s_out):
+                s.wait_stream(cur)
         for i, b0 in enumerate(range(0, b, chunk)):
             k = i % nslots
             dx, dc, dd, dout = bufs[k]
@@ -121,9 +129,15 @@ class HashEngine:
             with torch.cuda.stream(s_out):
                 out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
                 ev["out"][k].record(s_out)
-        for s in (s_in, s_comp, s_out):
-            cur.wait_stream(s)
+        if join_out:
+            self.join(cur)
         return out
+
+    def join(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Make `stream` (default: the current one) wait for every pipelined call."""
+        cur = stream or torch.cuda.current_stream(self.device)
+        for s in self._pipe_streams():
+            cur.wait_stream(s)
 
     def seed_device(self, rng_seed, first_index: int, batch: int, c: torch.Tensor,
                     d: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
@@ -146,7 +160,8 @@ class HashEngine:
 
     def hash_seeded_host(self, x: torch.Tensor, rng_seed, first_index: int = 0,
                          out: torch.Tensor | None = None, streams: int = 3,
-                         chunk: int | None = None) -> torch.Tensor:
+                         chunk: int | None = None, join_in: bool = True,
+                         join_out: bool = True) -> torch.Tensor:
         """run_pa's step end to end: key blocks x from (pinned) host memory, block
         first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
         derived on the GPU (only x crosses PCIe).
@@ -155,7 +170,7 @@ class HashEngine:
         Keccak-f calls), so the whole call's seeds are expanded by one launch on a
         stream of their own, into one of two alternating buffers: the next call's
         expansion runs beside this call's hashing.  H2D of x, hashing and D2H are
-        pipelined over `streams` slots as in hash_host.
+        pipelined over `streams` slots as in hash_host (join_in / join_out as there).
         """
         b = x.shape[0]
         if out is None:
@@ -168,8 +183,9 @@ class HashEngine:
         ev = self._slot_events(nslots)
         sc, sd, ev_free, ev_ready = self._seed_buffers(b)
         cur = torch.cuda.current_stream(self.device)
-        for s in (s_in, s_comp, s_out):
-            s.wait_stream(cur)
+        if join_in:
+            for s in (s_in, s_comp, s_out):
+                s.wait_stream(cur)
         # the expansion reads nothing of the caller's: it only waits for its buffer
         # (so it runs ahead, beside the previous call's hashing)
         s_seed.wait_event(ev_free)
@@ -193,8 +209,8 @@ class HashEngine:
                 out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
                 ev["out"][k].record(s_out)
         ev_free.record(s_comp)
-        for s in (s_in, s_comp, s_out):        # s_comp has waited for s_seed's launch
-            cur.wait_stream(s)
+        if join_out:                           # s_comp has waited for s_seed's launch
+            self.join(cur)
         return out
 
     def _seed_buffers(self, b: int):

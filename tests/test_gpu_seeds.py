@@ -115,3 +115,27 @@ def test_hash_seeded_host_matches_oracle(n, r):
     out = eng.hash_seeded_host(torch.from_numpy(x).pin_memory(), 9, first_index=40)
     torch.cuda.synchronize()
     assert [out[j].numpy().tobytes() for j in range(B)] == want
+
+
+def test_streamed_calls_without_joins():
+    # hash_host / hash_seeded_host chained with join_in / join_out off, one join() at the end
+    n, r, B = 100_000, 30_001, 6
+    rng = np.random.default_rng(3)
+    nb = (n + 7) // 8
+    xs = [rng.integers(0, 256, size=(B, nb), dtype=np.uint8) for _ in range(3)]
+    cs, ds = host_seeds(n, 4, 0, B)
+    c = np.frombuffer(b"".join(cs), np.uint8).reshape(B, nb)
+    d = np.frombuffer(b"".join(ds), np.uint8).reshape(B, nb)
+    eng = HashEngine(n, r, max_batch=2)
+    pc, pd = torch.from_numpy(c.copy()).pin_memory(), torch.from_numpy(d.copy()).pin_memory()
+    outs, souts = [], []
+    for i, x in enumerate(xs):
+        px = torch.from_numpy(x).pin_memory()
+        outs.append(eng.hash_host(px, pc, pd, join_in=i == 0, join_out=False))
+        souts.append(eng.hash_seeded_host(px, 4, 0, join_in=False, join_out=False))
+    eng.join()
+    torch.cuda.synchronize()
+    for x, o, so in zip(xs, outs, souts):
+        want = [oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r) for j in range(B)]
+        assert [o[j].numpy().tobytes() for j in range(B)] == want
+        assert [so[j].numpy().tobytes() for j in range(B)] == want
