@@ -33,3 +33,19 @@ s = pab.gen_seed(70, 3)
 pab.compress(x, s, 20)
 assert pab.mul(3**2000, 7**1500).value == 3**2000 * 7**1500
 print("sanitize script done")
+# seed expansion (lane-pair Keccak) + the seeded host path, LSF and MSF, ragged n
+for n, r, B, order in [(1089, 100, 3, _native.ORDER_LSF), (20_001, 777, 2, _native.ORDER_MSF)]:
+    nb = (n + 7) // 8
+    eng = HashEngine(n, r, order=order, max_batch=B)
+    c = torch.empty((B, nb), dtype=torch.uint8, device="cuda")
+    d = torch.empty_like(c)
+    eng.seed_device(9, 5, B, c, d)
+    torch.cuda.synchronize()
+    endian = "big" if order == _native.ORDER_MSF else "little"
+    for j in range(B):
+        sd = pab.gen_seed(n, pab.derive_block_seed(9, 5 + j))
+        assert c[j].cpu().numpy().tobytes() == sd.c.value.to_bytes(nb, endian)
+        assert d[j].cpu().numpy().tobytes() == sd.d.value.to_bytes(nb, endian)
+xs = rng.integers(0, 256, size=(2, 125_000), dtype=np.uint8)
+_native.hash_seeded_host(xs.tobytes(), 1_000_000, 500_000, 2, 0, first_index=3)
+print("seed paths done")
