@@ -704,6 +704,69 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
     // (+ twiddles w_R^(j*s)), then the top RS0 DIF stages of all M sub-columns with
     // shared table twiddles, and stores once to smem.
     constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+    constexpr int NK = 1 << RS0;
+    // operand rows >= R/2 are zero when kc <= L/2 (always for the hash): of the
+    // radix-M inputs (rows j + s R2, j = o + k 2^SLO0) only sub-columns s < M/2,
+    // and s = M/2 for j < R2/2 (k < NK/2), can be nonzero -- compile-time per
+    // (s, k), so their loads all issue before any use (ncu at 1e8: the first use
+    // of each load was 25% of stall samples) and the known zeros fold away.
+    if (ov.kc <= (L >> 1)) {
+      const uint2* src2 = reinterpret_cast<const uint2*>(ov.src);
+      for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+        const int t = task & (CT - 1), o = task >> lct;
+        uint2 raw[M][NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+#pragma unroll
+          for (int s = 0; s < M; ++s) {
+            raw[s][k] = make_uint2(0u, 0u);
+            if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
+              const int row = o + (k << SLO0) + s * R2;
+              const int gi = (row << lgC) + c0 + t;
+              if (STAGED) {  // staged raw words (last one already masked)
+                if (row < srows) raw[s][k] = stage[(row << lct) + t];
+              } else if (gi < ov.kc) {
+                if (ov.cw == 2) {
+                  raw[s][k] = __ldg(src2 + gi);
+                } else {
+                  raw[s][k].x = __ldg(ov.src + gi);
+                }
+              }
+            }
+          }
+        }
+        u32 v[M][NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int j = o + (k << SLO0);
+          u32 a[M];
+#pragma unroll
+          for (int s = 0; s < M; ++s) {
+            if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
+              const int gi = ((j + s * R2) << lgC) + c0 + t;
+              uint2 w = raw[s][k];
+              if (!STAGED && gi == ov.kc - 1) {
+                w.x &= ov.mlo;
+                w.y &= ov.mhi;
+              }
+              a[s] = coef_red<P>(w.x, w.y, ov.cw);
+            } else {
+              a[s] = 0u;
+            }
+          }
+          radix_m<P, M, false>(a);
+#pragma unroll
+          for (int s = 0; s < M; ++s)
+            v[s][k] = s ? shoup(a[s], __ldg(trad + j * s), PK<P>::p) : a[0];
+        }
+        dif_rt<P, RS0, SLO0, M>(v, twf + o);
+#pragma unroll
+        for (int s = 0; s < M; ++s)
+#pragma unroll
+          for (int k = 0; k < NK; ++k)
+            smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t] = v[s][k];
+      }
+    } else
     for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
       const int t = task & (CT - 1), o = task >> lct;
       u32 v[M][1 << RS0];
@@ -867,7 +930,10 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
 }
 
 template <int M, int LGR2, int LGC>
-__global__ void __maxnreg__(48) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
+#ifndef PAB_COLM3_FWD_REGS
+#define PAB_COLM3_FWD_REGS 64
+#endif
+__global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
   const FwdIdx ix = fwd_idx(job, lct);
 #define PAB_B(P_) colm_fwd_body<P_, M, LGR2, LGC>(job, tab, lct, ix.b, ix.op, ix.tile);
   PAB_PRIME_SWITCH(PAB_B, ix.prime)
