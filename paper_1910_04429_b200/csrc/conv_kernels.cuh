@@ -567,7 +567,6 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
   const u32* src = job.buf + (((long long)b * 2 + 1) * job.np + P) * L;
   u32* res = job.buf + (((long long)b * 2 + 0) * job.np + P) * L;
   const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
-  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
 
   if constexpr (PP.n == 1) {
     for (int t = threadIdx.x; t < CT; t += blockDim.x) {
@@ -578,7 +577,7 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
 #pragma unroll
       for (int k = 0; k < (1 << LGR); ++k) {
         const long long gi = ((long long)k << lgC) + c0 + t;
-        if (gi < job.nRes) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+        if (gi < job.nRes) res[gi] = red(red(v[k], PK<P>::two_p), PK<P>::p);  // scale is in the twiddles
       }
     }
   } else {
@@ -624,14 +623,14 @@ __device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTable
 #pragma unroll
         for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
           const int gi = ((o + (k << SLO0)) << lgC) + c0 + t;
-          if (gi < nres) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+          if (gi < nres) res[gi] = red(red(v[k], PK<P>::two_p), PK<P>::p);  // scale is in the twiddles
         }
       } else {
         dit_rt<P, RS0, SLO0>(v, twi + o);
 #pragma unroll
         for (int k = 0; k < (1 << RS0); ++k) {
           const int gi = ((o + (k << SLO0)) << lgC) + c0 + t;
-          if (gi < nres) res[gi] = red(shoup(v[k], sc, sc_sh, PK<P>::p), PK<P>::p);
+          if (gi < nres) res[gi] = red(red(v[k], PK<P>::two_p), PK<P>::p);  // scale is in the twiddles
         }
       }
     }
@@ -853,7 +852,6 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
   u32* res = job.buf + (((long long)b * 2 + 0) * job.np + P) * L;
   const uint2* twi = tab.stw + (P * 2 + 1) * kTwN;
   const uint2* trad = tab.trad + (P * 2 + 1) * tab.tstride;
-  const u32 sc = tab.scale[P], sc_sh = tab.scale_sh[P];
   // first pow2 DIT pass (stages 0..RSL-1) from global
   constexpr int RSL = PP.rs[PP.n - 1];
   {
@@ -902,7 +900,7 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
 #pragma unroll
         for (int s = 0; s < M; ++s) {
           const int gi = ((j + s * R2) << lgC) + c0 + t;
-          if (gi < nres) res[gi] = red(shoup(a[s], sc, sc_sh, PK<P>::p), PK<P>::p);
+          if (gi < nres) res[gi] = red(a[s], PK<P>::p);  // [0, 2p) -> canonical; scale in the twiddles
         }
       }
     }
@@ -912,7 +910,7 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
     colm_pass<P, M, LGR2, PP.rs[0], PP.slo[0], false>(smem, lct, twi);
     __syncthreads();
   }
-  // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT, scale -> residues
+  // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT -> canonical residues
   for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
     const int t = task & (CT - 1), j = task >> lct;
     u32 a[M];
@@ -924,7 +922,7 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
 #pragma unroll
     for (int s = 0; s < M; ++s) {
       const int gi = ((j + s * R2) << lgC) + c0 + t;
-      if (gi < nres) res[gi] = red(shoup(a[s], sc, sc_sh, PK<P>::p), PK<P>::p);
+      if (gi < nres) res[gi] = red(a[s], PK<P>::p);  // [0, 2p) -> canonical; scale in the twiddles
     }
   }
 }

@@ -264,6 +264,14 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
     pl.scale[i] = pl.scale_sh[i] = 0;
     if ((p - 1) % L != 0) continue;  // a cw = 1 length beyond this prime's 2-adicity
     const u64 r32 = ((u64)1 << 32) % p;
+    // L^-1 * 2^32: undoes the length and the Montgomery factor of the pointwise
+    // product.  The four-step path folds it into the inverse four-step twiddles
+    // (thi and tw4, dir 1), so the inverse column pass only canonicalises; the
+    // single-CTA path (R == 1) applies pl.scale itself.
+    const u64 linv = inv_mod((u32)(L % p), p);
+    const u64 sc = linv * r32 % p;
+    pl.scale[i] = (u32)sc;
+    pl.scale_sh[i] = shoup_of(pl.scale[i], p);
     for (int dir = 0; dir < 2; ++dir) {
       const size_t pd = (size_t)i * 2 + dir;
       const u32 wL = root_of(i, L, dir);
@@ -284,15 +292,12 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
         x = x * wL % p;
       }
       const u64 step = powmod(wL, kTwN, p);
-      x = 1;
+      x = (dir == 1 && R > 1) ? sc : 1;
       for (int j = 0; j < pl.thi_stride; ++j) {
         thi[pd * pl.thi_stride + j] = make_uint2((u32)x, shoup_of((u32)x, p));
         x = x * step % p;
       }
     }
-    const u64 linv = inv_mod((u32)(L % p), p);
-    pl.scale[i] = (u32)(linv * r32 % p);
-    pl.scale_sh[i] = shoup_of(pl.scale[i], p);
   }
   int rc;
   if ((rc = upload((void**)&pl.tlo_m, tlo.data(), tlo.size() * sizeof(u32)))) return rc;
@@ -312,7 +317,7 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
           // column frequency of storage row q (conv_kernels.cuh: row_k1)
           const int k1 = (q >> geo.lgR) + geo.m * bitrev(q & ((1 << geo.lgR) - 1), geo.lgR);
           const u64 step = powmod(wL, (u64)k1, p);
-          u64 x = 1;
+          u64 x = dir == 1 ? pl.scale[i] : 1;  // the inverse carries L^-1 * 2^32
           for (int c = 0; c < C; ++c) {
             t[(size_t)q * C + c] = make_uint2((u32)x, shoup_of((u32)x, p));
             x = x * step % p;
