@@ -19,6 +19,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pa_b200.h"
@@ -36,7 +37,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<int> g_force_cw{0};  // test hook (pab_force_coef_words): 0 = automatic
-constexpr int kTw4MaxLg = 20;  // full four-step twiddle tables up to L = 2^20 (80 L bytes <= 80 MiB)
+constexpr int kTw4MaxLg = 22;  // full four-step twiddle tables up to L = 2^22 (80 L bytes <= 320 MiB; at 3*2^20 k_row -3%)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -307,24 +308,29 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   // full four-step twiddle tables (L <= 2^kTw4MaxLg): 80 L bytes, read once per launch
   if (R > 1 && L <= ((u64)1 << kTw4MaxLg)) {
     std::vector<uint2> t4((size_t)kNumPrimes * 2 * L);
+    // one host thread per (prime, direction): 10 x L entries (0.3 s serial at 3 * 2^20)
+    std::vector<std::thread> workers;
     for (int i = 0; i < kNumPrimes; ++i) {
       const u32 p = kPrimes[i];
       if ((p - 1) % L != 0) continue;
       for (int dir = 0; dir < 2; ++dir) {
-        const u32 wL = root_of(i, L, dir);
-        uint2* t = &t4[((size_t)i * 2 + dir) * L];
-        for (int q = 0; q < R; ++q) {
-          // column frequency of storage row q (conv_kernels.cuh: row_k1)
-          const int k1 = (q >> geo.lgR) + geo.m * bitrev(q & ((1 << geo.lgR) - 1), geo.lgR);
-          const u64 step = powmod(wL, (u64)k1, p);
-          u64 x = dir == 1 ? pl.scale[i] : 1;  // the inverse carries L^-1 * 2^32
-          for (int c = 0; c < C; ++c) {
-            t[(size_t)q * C + c] = make_uint2((u32)x, shoup_of((u32)x, p));
-            x = x * step % p;
+        workers.emplace_back([&, i, p, dir] {
+          const u32 wL = root_of(i, L, dir);
+          uint2* t = &t4[((size_t)i * 2 + dir) * L];
+          for (int q = 0; q < R; ++q) {
+            // column frequency of storage row q (conv_kernels.cuh: row_k1)
+            const int k1 = (q >> geo.lgR) + geo.m * bitrev(q & ((1 << geo.lgR) - 1), geo.lgR);
+            const u64 step = powmod(wL, (u64)k1, p);
+            u64 x = dir == 1 ? pl.scale[i] : 1;  // the inverse carries L^-1 * 2^32
+            for (int c = 0; c < C; ++c) {
+              t[(size_t)q * C + c] = make_uint2((u32)x, shoup_of((u32)x, p));
+              x = x * step % p;
+            }
           }
-        }
+        });
       }
     }
+    for (auto& w : workers) w.join();
     if ((rc = upload((void**)&pl.tw4, t4.data(), t4.size() * sizeof(uint2)))) return rc;
   }
   auto res = ds->plans.emplace(key, pl);
