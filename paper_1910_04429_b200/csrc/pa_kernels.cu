@@ -940,7 +940,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    row_kernel(job.lgC, false)<<<dim3((unsigned)(R >> lnr), job.batch, job.np), 128, smr,
+    row_kernel(job.lgC, false)<<<dim3(job.batch, (unsigned)(R >> lnr), job.np), 128, smr,
                                  st>>>(job, tab, lnr);
   }
   {
