@@ -15,7 +15,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpa_b200.so")
+LIB_PATH = os.environ.get("PAB_LIB") or os.path.join(_HERE, "_lib", "libpa_b200.so")  # PAB_LIB: dev builds
 
 PAB_OK = 0
 PAB_EINVAL = -1
