@@ -103,6 +103,20 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
                   uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device);
 
 /*
+ * One batch hashed with its NTT primes split over several GPUs (SURVEY.md
+ * §8f: single-block multi-GPU).  The convolution modulo each prime is
+ * independent, so share s of `ndev` computes the residues for its contiguous
+ * run of primes on devices[s]; the other shares' residue slots are then copied
+ * to devices[0] (peer to peer over NVLink where the pair allows it) for the
+ * CRT + carry.  Lowers the latency of one large block; throughput stays best
+ * with whole blocks per GPU (pab_hash_batch).  Host buffers as pab_hash_host;
+ * a device may repeat (its shares run on separate streams).  Blocks until done.
+ */
+int pab_hash_host_split(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
+                        uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out,
+                        const int* devices, int ndev);
+
+/*
  * Seed expansion on the device (SHAKE-256): for j < batch, the hash-family
  * member of block i = first_index + j exactly as run_pa derives it,
  *   gen_seed(n, derive_block_seed(master, i))          pkg/src/modpa/pa.py:156-172

@@ -40,6 +40,9 @@ SIGNATURES = {
                                       ctypes.c_uint64, _u8p, ctypes.c_size_t, _u8p]),
     "pab_hash_host": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_int]),
+    "pab_hash_host_split": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_uint32, ctypes.c_int, _u8p,
+                                           ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     "pab_seed_expand": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                        ctypes.c_uint64, ctypes.c_int, _u8p, _u8p,
                                        ctypes.c_uint64, _u8p]),
@@ -109,6 +112,18 @@ def hash_host(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
     dev = _device() if device is None else device
     out = ctypes.create_string_buffer(batch * ((r + 7) // 8))
     check(lib.pab_hash_host(x, c, d, n, r, batch, order, out, dev))
+    return out.raw
+
+
+def hash_host_split(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
+                    order: int = ORDER_LSF, devices: list[int] | None = None) -> bytes:
+    """As hash_host, with the NTT primes of the convolution split over `devices`
+    (devices[0] does the CRT + carry); a device may repeat."""
+    lib = load()
+    devs = [_device()] if not devices else list(devices)
+    arr = (ctypes.c_int * len(devs))(*devs)
+    out = ctypes.create_string_buffer(batch * ((r + 7) // 8))
+    check(lib.pab_hash_host_split(x, c, d, n, r, batch, order, out, arr, len(devs)))
     return out.raw
 
 

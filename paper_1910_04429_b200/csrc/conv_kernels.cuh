@@ -111,7 +111,7 @@ struct FwdIdx {
 __device__ __forceinline__ FwdIdx fwd_idx(const ConvJob& job, int lct) {
   const unsigned tc = 1u << (job.lgC - lct);
   const unsigned per_block = 2u * tc;  // CTAs of one (block, prime)
-  const unsigned span = per_block * (unsigned)job.np * (unsigned)job.fwd_chunk;
+  const unsigned span = per_block * (unsigned)job.pn * (unsigned)job.fwd_chunk;
   const unsigned id = blockIdx.x;
   const unsigned c = id / span;
   const unsigned local = id - c * span;
@@ -119,8 +119,9 @@ __device__ __forceinline__ FwdIdx fwd_idx(const ConvJob& job, int lct) {
   const int nb = min(job.fwd_chunk, job.batch - b0);
   const unsigned per_prime = per_block * (unsigned)nb;
   FwdIdx r;
-  r.prime = (int)(local / per_prime);
-  const unsigned rem = local - (unsigned)r.prime * per_prime;
+  const unsigned pi = local / per_prime;
+  r.prime = job.p0 + (int)pi;
+  const unsigned rem = local - pi * per_prime;
   r.b = b0 + (int)(rem / per_block);
   const unsigned w = rem - (rem / per_block) * per_block;
   r.op = (int)(w / tc);
@@ -170,7 +171,7 @@ __device__ __forceinline__ u32 coef_staged(const uint2* stage, int row, int t, i
   return coef_red<P>(w.x, w.y, cw);
 }
 
-// conv kernels run one prime per grid index IDX (job.np of them).  Kernels
+// conv kernels run one prime per grid index IDX (primes p0 .. p0 + pn - 1).  Kernels
 // without cross-prime data reuse (row, inverse column) put the prime in the
 // slowest grid dimension so CTAs resident together run the same prime's
 // code: one body is ~20-40 KB of straight-line SASS, and mixing primes on an
@@ -443,7 +444,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
 template <int LGC, bool SMALL>
 __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
 #define PAB_B(P_) row_body<P_, LGC, SMALL>(job, tab, lnr);
-  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+  PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
 }
 
@@ -943,7 +944,7 @@ __global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob
 template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
 #define PAB_B(P_) colm_inv_body<P_, M, LGR2, LGC>(job, tab, lct);
-  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+  PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
 }
 
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
   stage_operand(ov, stage, rows, lct, LGC, tile << lct);  // (its barrier covers s_tw too)
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
-    if (P < job.np) {
+    if (P >= job.p0 && P < job.p0 + job.pn) {
       col_fwd_body<P, LGR, LGC, true>(job, tab, lct, b, op, tile, stage, s_tw + P * NTW);
       __syncthreads();  // the next prime reuses the transform panel
     }
@@ -1005,7 +1006,7 @@ __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int 
   stage_operand(ov, stage, rows, lct, LGC, tile << lct);
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
-    if (P < job.np) {
+    if (P >= job.p0 && P < job.p0 + job.pn) {
       colm_fwd_body<P, M, LGR2, LGC, true>(job, tab, lct, b, op, tile, stage, rows);
       __syncthreads();  // the next prime reuses the transform panel
     }
@@ -1015,7 +1016,7 @@ __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int 
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
 #define PAB_B(P_) col_inv_body<P_, LGR, LGC>(job, tab, lct);
-  PAB_PRIME_SWITCH(PAB_B, blockIdx.z)
+  PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
 }
 

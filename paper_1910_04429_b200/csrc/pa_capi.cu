@@ -167,12 +167,24 @@ struct HostCtx {  // cached buffers for the host-pointer entry points
   std::mutex mu;
 };
 
+struct SplitSlot {  // one prime share of pab_hash_host_split on this device
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  uint8_t* io = nullptr;
+  size_t io_bytes = 0;
+};
+
 struct DevState {
   bool ready = false;
   uint2* stw = nullptr;
   std::map<int, Plan> plans;  // keyed by m * 64 + lg
   HostCtx host;
+  std::vector<std::unique_ptr<SplitSlot>> split;  // guarded by g_split_mu
 };
+
+std::mutex g_split_mu;  // pab_hash_host_split calls run one at a time
 
 std::mutex g_mu;
 std::map<int, std::unique_ptr<DevState>> g_dev;
@@ -474,6 +486,8 @@ ConvJob make_job(const Layout& ly, void* ws, const Mode& md, int batch) {
   j.batch = batch;
   j.cw = md.cw;
   j.np = md.np;
+  j.p0 = 0;
+  j.pn = md.np;
   j.m = geo.m;
   j.lg = geo.lg;
   j.lgR = geo.lgR;
@@ -492,6 +506,104 @@ ConvJob make_job(const Layout& ly, void* ws, const Mode& md, int batch) {
 bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)) == 0; }
 
 }  // namespace
+
+// The hash over a workspace.  mode kFull: convolution over every prime + carry;
+// kConvOnly: convolution over primes [p0, p0 + pn) into the workspace's residue
+// slots (one chunk: the batch must fit); kCarryOnly: carry from residues
+// already in the workspace (all primes).  The split modes serve
+// pab_hash_host_split (primes over GPUs).
+enum HashMode { kFull = 0, kConvOnly = 1, kCarryOnly = 2 };
+static int hash_batch_impl(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t in_stride,
+                           uint64_t n_bits, uint64_t r_bits, uint32_t batch, int byte_order,
+                           uint8_t* out, uint64_t out_stride, void* workspace,
+                           size_t workspace_bytes, void* stream, int p0, int pn, int mode) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, r_bits, &g);
+  if (rc) return rc;
+  if (batch == 0) return PAB_OK;
+  if (!x || !c || !d || !out || !workspace) return fail(PAB_EINVAL, "null pointer argument");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
+  if (in_stride < nbytes || out_stride < rbytes)
+    return fail(PAB_EINVAL, "stride smaller than the block byte length");
+  DevState* ds;
+  if ((rc = current_device(&ds))) return rc;
+  const Plan* pl;
+  if ((rc = get_plan(ds, g.md.geo, &pl))) return rc;
+  const PlanTables tab = tables_of(ds, pl);
+  cudaStream_t st = (cudaStream_t)stream;
+  // blocks per chunk that fit the workspace
+  u64 chunk = batch < kMaxChunk ? batch : kMaxChunk;  // grid y/z limits
+  while (chunk > 0 && layout_for(g.K, g.md.geo.L, g.K, g.mw, chunk, g.md.np).total > workspace_bytes)
+    chunk /= 2;
+  if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
+  if (mode != kFull && chunk < batch)
+    return fail(PAB_EINVAL, "split hashing needs the whole batch in one workspace");
+  const int msf = byte_order == PAB_ORDER_MSF;
+  // LSF blocks whose words can be read in place (the common case): no pack kernel
+  // (64-bit coefficients are read as 8-byte words: whole, 8-byte aligned rows)
+  const u64 al = 4 * (u64)g.md.cw;
+  const bool direct_in = !msf && nbytes % al == 0 && in_stride % al == 0 && aligned(x, al) &&
+                         aligned(c, al) && aligned(d, al);
+  const bool direct_out = !msf && out_stride % 4 == 0 && aligned(out, 4);
+  const u32 mask = (n_bits & 31) ? ((1u << (n_bits & 31)) - 1u) : 0xFFFFFFFFu;
+  for (u64 b0 = 0; b0 < batch; b0 += chunk) {
+    const int nb = (int)((batch - b0) < chunk ? (batch - b0) : chunk);
+    const Layout ly = layout_for(g.K, g.md.geo.L, g.K, g.mw, nb, g.md.np);
+    ConvJob job = make_job(ly, workspace, g.md, nb);
+    job.p0 = p0;
+    job.pn = pn;
+    job.kA = job.kX = job.kD = (long long)g.K;
+    job.maskA = job.maskX = job.maskD = mask;
+    job.nT = (long long)g.K;
+    job.nRes = (long long)g.KC;
+    job.n_mod_bits = (long long)n_bits;
+    job.shift = (long long)(n_bits - r_bits);
+    job.mw = (long long)g.mw;
+    if (mode != kConvOnly)
+      CK(cudaMemsetAsync((char*)workspace + ly.off_state, 0, ly.total - ly.off_state, st), "memset");
+    if (direct_in) {
+      job.srcA = (const u32*)(c + b0 * in_stride);
+      job.srcX = (const u32*)(x + b0 * in_stride);
+      job.srcD = (const u32*)(d + b0 * in_stride);
+      job.src_stride = (long long)(in_stride / 4);
+    } else {
+      u32* words = (u32*)((char*)workspace + ly.off_words);
+      const long long ws = (long long)ly.in_stride;
+      if (mode != kCarryOnly) {
+        launch_pack(c + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words,
+                    3 * ws, (long long)g.K, st);
+        launch_pack(x + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
+                    words + ws, 3 * ws, (long long)g.K, st);
+      }
+      if (mode != kConvOnly)
+        launch_pack(d + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
+                    words + 2 * ws, 3 * ws, (long long)g.K, st);
+      job.srcA = words;
+      job.srcX = words + ws;
+      job.srcD = words + 2 * ws;
+      job.src_stride = 3 * ws;
+    }
+    if (direct_out) {
+      job.out_words = nullptr;
+      job.out_bytes = out + b0 * out_stride;
+      job.out_stride = (long long)out_stride;
+      job.rbytes = (long long)rbytes;
+    }
+    if (mode != kCarryOnly) launch_conv(job, tab, st);
+    if (mode == kConvOnly) {
+      CK(cudaGetLastError(), "kernel launch");
+      continue;
+    }
+    launch_carry(job, st);
+    if (!direct_out)
+      launch_unpack(job.out_words, job.mw, (long long)r_bits, msf, nb, out + b0 * out_stride,
+                    (long long)out_stride, st);
+    CK(cudaGetLastError(), "kernel launch");
+  }
+  return PAB_OK;
+}
 
 // ================================================================== C ABI
 extern "C" {
@@ -539,77 +651,8 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
   HashGeo g;
   int rc = hash_geo(n_bits, r_bits, &g);
   if (rc) return rc;
-  if (batch == 0) return PAB_OK;
-  if (!x || !c || !d || !out || !workspace) return fail(PAB_EINVAL, "null pointer argument");
-  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
-    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
-  const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
-  if (in_stride < nbytes || out_stride < rbytes)
-    return fail(PAB_EINVAL, "stride smaller than the block byte length");
-  DevState* ds;
-  if ((rc = current_device(&ds))) return rc;
-  const Plan* pl;
-  if ((rc = get_plan(ds, g.md.geo, &pl))) return rc;
-  const PlanTables tab = tables_of(ds, pl);
-  cudaStream_t st = (cudaStream_t)stream;
-  // blocks per chunk that fit the workspace
-  u64 chunk = batch < kMaxChunk ? batch : kMaxChunk;  // grid y/z limits
-  while (chunk > 0 && layout_for(g.K, g.md.geo.L, g.K, g.mw, chunk, g.md.np).total > workspace_bytes)
-    chunk /= 2;
-  if (chunk == 0) return fail(PAB_EINVAL, "workspace too small for one block");
-  const int msf = byte_order == PAB_ORDER_MSF;
-  // LSF blocks whose words can be read in place (the common case): no pack kernel
-  // (64-bit coefficients are read as 8-byte words: whole, 8-byte aligned rows)
-  const u64 al = 4 * (u64)g.md.cw;
-  const bool direct_in = !msf && nbytes % al == 0 && in_stride % al == 0 && aligned(x, al) &&
-                         aligned(c, al) && aligned(d, al);
-  const bool direct_out = !msf && out_stride % 4 == 0 && aligned(out, 4);
-  const u32 mask = (n_bits & 31) ? ((1u << (n_bits & 31)) - 1u) : 0xFFFFFFFFu;
-  for (u64 b0 = 0; b0 < batch; b0 += chunk) {
-    const int nb = (int)((batch - b0) < chunk ? (batch - b0) : chunk);
-    const Layout ly = layout_for(g.K, g.md.geo.L, g.K, g.mw, nb, g.md.np);
-    ConvJob job = make_job(ly, workspace, g.md, nb);
-    job.kA = job.kX = job.kD = (long long)g.K;
-    job.maskA = job.maskX = job.maskD = mask;
-    job.nT = (long long)g.K;
-    job.nRes = (long long)g.KC;
-    job.n_mod_bits = (long long)n_bits;
-    job.shift = (long long)(n_bits - r_bits);
-    job.mw = (long long)g.mw;
-    CK(cudaMemsetAsync((char*)workspace + ly.off_state, 0, ly.total - ly.off_state, st), "memset");
-    if (direct_in) {
-      job.srcA = (const u32*)(c + b0 * in_stride);
-      job.srcX = (const u32*)(x + b0 * in_stride);
-      job.srcD = (const u32*)(d + b0 * in_stride);
-      job.src_stride = (long long)(in_stride / 4);
-    } else {
-      u32* words = (u32*)((char*)workspace + ly.off_words);
-      const long long ws = (long long)ly.in_stride;
-      launch_pack(c + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words,
-                  3 * ws, (long long)g.K, st);
-      launch_pack(x + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb, words + ws,
-                  3 * ws, (long long)g.K, st);
-      launch_pack(d + b0 * in_stride, (long long)in_stride, (long long)n_bits, msf, nb,
-                  words + 2 * ws, 3 * ws, (long long)g.K, st);
-      job.srcA = words;
-      job.srcX = words + ws;
-      job.srcD = words + 2 * ws;
-      job.src_stride = 3 * ws;
-    }
-    if (direct_out) {
-      job.out_words = nullptr;
-      job.out_bytes = out + b0 * out_stride;
-      job.out_stride = (long long)out_stride;
-      job.rbytes = (long long)rbytes;
-    }
-    launch_conv(job, tab, st);
-    launch_carry(job, st);
-    if (!direct_out)
-      launch_unpack(job.out_words, job.mw, (long long)r_bits, msf, nb, out + b0 * out_stride,
-                    (long long)out_stride, st);
-    CK(cudaGetLastError(), "kernel launch");
-  }
-  return PAB_OK;
+  return hash_batch_impl(x, c, d, in_stride, n_bits, r_bits, batch, byte_order, out, out_stride,
+                         workspace, workspace_bytes, stream, 0, g.md.np, kFull);
 }
 
 static int host_ensure(HostCtx& h, size_t ws_bytes, size_t io_bytes) {
@@ -759,6 +802,123 @@ int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uin
                        h.stream),
      "D2H out");
   CK(cudaStreamSynchronize(h.stream), "synchronize");
+  return PAB_OK;
+}
+
+int pab_hash_host_split(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
+                        uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out,
+                        const int* devices, int ndev) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, r_bits, &g);
+  if (rc) return rc;
+  if (batch == 0) return PAB_OK;
+  if (!x || !c || !d || !out) return fail(PAB_EINVAL, "null pointer argument");
+  if (!devices || ndev < 1) return fail(PAB_EINVAL, "need at least one device");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  const int np = g.md.np;
+  const int nsh = ndev < np ? ndev : np;  // shares of the primes
+  const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
+  const u64 in_stride = round_up(nbytes, 16), out_stride = round_up(rbytes, 16);
+  const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, batch);
+  if (ws_bytes == 0) return fail(PAB_EINVAL, "no workspace size for this block");
+  const size_t io_bytes = (size_t)batch * (3 * in_stride + out_stride);
+  const Layout ly = layout_for(g.K, g.md.geo.L, g.K, g.mw, batch, np);
+  std::lock_guard<std::mutex> lk(g_split_mu);
+  struct Share {
+    int dev, p0, pn;
+    SplitSlot* slot;
+  };
+  std::vector<Share> sh;
+  std::map<int, int> used;  // shares already placed on a device
+  for (int s = 0; s < nsh; ++s) {
+    Share e;
+    e.dev = devices[s];
+    e.p0 = (int)((long long)s * np / nsh);
+    e.pn = (int)((long long)(s + 1) * np / nsh) - e.p0;
+    CK(cudaSetDevice(e.dev), "cudaSetDevice");
+    DevState* ds;
+    if ((rc = ensure_device(e.dev, &ds))) return rc;
+    const int k = used[e.dev]++;
+    while ((int)ds->split.size() <= k) ds->split.emplace_back(new SplitSlot());
+    SplitSlot& sl = *ds->split[k];
+    if (!sl.stream) CK(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking), "stream");
+    if (!sl.done) CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming), "event");
+    if (sl.ws_bytes < ws_bytes) {
+      if (sl.ws) cudaFree(sl.ws);
+      sl.ws = nullptr;
+      sl.ws_bytes = 0;
+      CK(cudaMalloc(&sl.ws, ws_bytes), "split workspace alloc");
+      sl.ws_bytes = ws_bytes;
+    }
+    if (sl.io_bytes < io_bytes) {
+      if (sl.io) cudaFree(sl.io);
+      sl.io = nullptr;
+      sl.io_bytes = 0;
+      CK(cudaMalloc(&sl.io, io_bytes), "split io alloc");
+      sl.io_bytes = io_bytes;
+    }
+    if (e.dev != devices[0]) {  // residues go straight over NVLink when the pair allows it
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[0], e.dev);
+      if (can) {
+        CK(cudaSetDevice(devices[0]), "cudaSetDevice");
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(e.dev, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+          return cuda_fail(pe, "enable peer access");
+        cudaGetLastError();
+      }
+    }
+    e.slot = &sl;
+    sh.push_back(e);
+  }
+  // each share: its operands host -> its device, the convolution over its primes
+  for (int s = 0; s < nsh; ++s) {
+    const Share& e = sh[s];
+    CK(cudaSetDevice(e.dev), "cudaSetDevice");
+    SplitSlot& sl = *e.slot;
+    uint8_t* dx = sl.io;
+    uint8_t* dc = dx + batch * in_stride;
+    uint8_t* dd = dc + batch * in_stride;
+    uint8_t* dout = dd + batch * in_stride;
+    CK(cudaMemcpy2DAsync(dx, in_stride, x, nbytes, nbytes, batch, cudaMemcpyHostToDevice,
+                         sl.stream), "H2D x");
+    CK(cudaMemcpy2DAsync(dc, in_stride, c, nbytes, nbytes, batch, cudaMemcpyHostToDevice,
+                         sl.stream), "H2D c");
+    if (s == 0)
+      CK(cudaMemcpy2DAsync(dd, in_stride, d, nbytes, nbytes, batch, cudaMemcpyHostToDevice,
+                           sl.stream), "H2D d");
+    if ((rc = hash_batch_impl(dx, dc, dd, in_stride, n_bits, r_bits, batch, byte_order, dout,
+                              out_stride, sl.ws, sl.ws_bytes, sl.stream, e.p0, e.pn, kConvOnly)))
+      return rc;
+    CK(cudaEventRecord(sl.done, sl.stream), "event record");
+  }
+  // home (share 0): gather the other shares' residue slots, then CRT + carry
+  const Share& h = sh[0];
+  CK(cudaSetDevice(h.dev), "cudaSetDevice");
+  SplitSlot& hs = *h.slot;
+  const u64 L = g.md.geo.L;
+  const size_t slot_bytes = (size_t)g.KC * 4;  // residues below K' are all the carry reads
+  for (int s = 1; s < nsh; ++s) {
+    const Share& e = sh[s];
+    CK(cudaStreamWaitEvent(hs.stream, e.slot->done, 0), "stream wait");
+    for (u32 b = 0; b < batch; ++b)
+      for (int P = e.p0; P < e.p0 + e.pn; ++P) {
+        const size_t off = ly.off_buf + (((size_t)b * 2 + 0) * np + P) * L * 4;
+        CK(cudaMemcpyPeerAsync((char*)hs.ws + off, h.dev, (const char*)e.slot->ws + off, e.dev,
+                               slot_bytes, hs.stream), "residue gather");
+      }
+  }
+  uint8_t* hx = hs.io;
+  uint8_t* hc = hx + batch * in_stride;
+  uint8_t* hd = hc + batch * in_stride;
+  uint8_t* hout = hd + batch * in_stride;
+  if ((rc = hash_batch_impl(hx, hc, hd, in_stride, n_bits, r_bits, batch, byte_order, hout,
+                            out_stride, hs.ws, hs.ws_bytes, hs.stream, 0, np, kCarryOnly)))
+    return rc;
+  CK(cudaMemcpy2DAsync(out, rbytes, hout, out_stride, rbytes, batch, cudaMemcpyDeviceToHost,
+                       hs.stream), "D2H out");
+  CK(cudaStreamSynchronize(hs.stream), "synchronize");
   return PAB_OK;
 }
 

@@ -881,7 +881,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   if (job.m == 1 && job.lgR == 0) {
     const size_t sm = (size_t)sm_len(job.lgC) * 2 * 4;
     prof::Scope ps_("k_row_single", st);
-    row_kernel(job.lgC, true)<<<dim3(1, job.batch, job.np), threads, sm, st>>>(job, tab, 0);
+    row_kernel(job.lgC, true)<<<dim3(1, job.batch, job.pn), threads, sm, st>>>(job, tab, 0);
     return;
   }
   const long long R = (long long)job.m << job.lgR;
@@ -928,7 +928,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     const long long kmax = job.kA > job.kX ? job.kA : job.kX;
     long long chunk = (32ll << 20) / (8 * kmax);
     jf.fwd_chunk = (int)(chunk < 1 ? 1 : (chunk > job.batch ? job.batch : chunk));
-    const unsigned ctas = (1u << (job.lgC - lct)) * 2u * (unsigned)job.np * (unsigned)job.batch;
+    const unsigned ctas = (1u << (job.lgC - lct)) * 2u * (unsigned)job.pn * (unsigned)job.batch;
     cf<<<ctas, cf_threads, smc, st>>>(jf, tab, lct);
   }
   // rows: 4K words of rows (A+X: 8K words) per 128-thread CTA -- the same
@@ -940,7 +940,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    row_kernel(job.lgC, false)<<<dim3(job.batch, (unsigned)(R >> lnr), job.np), 128, smr,
+    row_kernel(job.lgC, false)<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), 128, smr,
                                  st>>>(job, tab, lnr);
   }
   {
@@ -950,7 +950,7 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     const int xi = job.m == 1 && lct >= 6 ? 1 : 0;
     const int lci = lct - xi;
     const size_t smi = (size_t)job.m * sm_len(job.lgR) * (1u << lci) * 4;
-    ci<<<dim3(1u << (job.lgC - lci), job.batch, job.np), ct_threads >> xi, smi, st>>>(job, tab,
+    ci<<<dim3(1u << (job.lgC - lci), job.batch, job.pn), ct_threads >> xi, smi, st>>>(job, tab,
                                                                                    lci);
   }
 }

@@ -28,7 +28,9 @@ struct PlanTables {
 struct ConvJob {
   int batch;
   int cw;                      // words per coefficient: 2 (five primes) or 1 (three primes)
-  int np;                      // primes (grid.y of the conv kernels): 5 if cw == 2 else 3
+  int np;                      // primes (buffer layout, CRT): 5 if cw == 2 else 3
+  int p0, pn;                  // primes [p0, p0 + pn) this job's convolution computes
+                               // (all of them unless the primes are split over GPUs)
   int m;                       // radix of the column length: L = m * 2^lg
   int lg, lgR, lgC;            // R = m * 2^lgR rows (columns of length R), C = 2^lgC
   long long L;                 // transform length (R = 1: single-CTA path)
