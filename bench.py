@@ -14,6 +14,7 @@ scaling (blocks shard by index, no collective on the data path).
            H2D of x, c, d and D2H of the keys inside the timed region.
 `e2e_run_pa`: run_pa's scope (n <= 1e7): only the key blocks x cross PCIe; each
            block's (c, d) is expanded on the GPU (SHAKE-256) beside the hashing.
+`ratio_sweep` (--config C5): device-resident Mbps at m/n = 0.1, 0.5, 0.9.
 `--impl reference`: the reference's CPU algorithm (the C port under oracle/,
            all host threads, rank 0 only) on a bounded sample of the workload.
 """
@@ -353,8 +354,27 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
     e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) \
         if n <= 10_000_000 else None
 
+    # C5's compression-ratio sweep (BASELINE configs[4]: m/n in {0.1, 0.5, 0.9}),
+    # device-resident, same blocks; the output length only changes the carry's writes
+    sweep = None
+    if len(cfg["ms"]) > 1:
+        sweep = []
+        for rr in cfg["ms"]:
+            e_r = HashEngine(n, rr, max_batch=cfg.get("chunk", per_rank))
+            o_r = e_r.hash_device(dx, dc, dd)
+            k = max(3, min(args.steps, 10))
+            ms_r, _ = time_device(e_r, dx, dc, dd, o_r, k, max(3, args.warmup // 2), dist,
+                                  profile=False)
+            ms_r = max_over_ranks(ms_r / k, dist)
+            sr = step_roofline(n, rr, per_rank, ms_r)
+            sweep.append({"r": rr, "ratio": round(rr / n, 3),
+                          "value": round(bits_step / (ms_r * 1e-3) / 1e6, 1),
+                          "ms_per_step": round(ms_r, 4), "steps": k,
+                          "step_roofline_frac": sr["frac"] if sr else None})
+            del e_r, o_r
+
     res = {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
-           "e2e_seeded": e2e_seeded,
+           "e2e_seeded": e2e_seeded, "ratio_sweep": sweep,
            "out": first_out, "per_rank": per_rank, "n": n, "r": r, "eng": eng,
            "dist": dist, "seeds": seeds}
     return res
@@ -540,7 +560,7 @@ def main():
         cfg["e2e_chunk"] = 2
         if args.config == "C5":
             cfg["seeds"] = tuple(range(16))  # 16 blocks/rank per step (1.6 Gbit)
-            cfg["ms"] = (50_000_000,)
+            cfg["ms"] = (50_000_000, 10_000_000, 90_000_000)  # main line at m/n = 0.5, then the sweep
     elif args.config == "C3":
         cfg["cpu_blocks"] = 16
         cfg["e2e_chunk"] = 8
@@ -610,6 +630,8 @@ def main():
         }
         if extra:
             line["n1e8"] = extra
+        if res.get("ratio_sweep"):
+            line["ratio_sweep"] = res["ratio_sweep"]
         print(json.dumps(line), flush=True)
     if res["dist"]:
         res["dist"].destroy_process_group()
