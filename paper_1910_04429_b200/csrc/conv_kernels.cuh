@@ -142,8 +142,10 @@ __device__ __forceinline__ void cp_async8(void* s, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((u32)__cvta_generic_to_shared(s)),
                "l"(g));
 }
-__device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, int rows, int lct,
+template <int LCT = -1>
+__device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, int rows, int lct_in,
                                               int lgC, int c0) {
+  const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
   for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
     const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
@@ -453,14 +455,18 @@ __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int ln
 // smem as s[sm_idx(row) * CT + t]; lanes walk columns (coalesced, twiddle
 // broadcast).  Forward: operand words -> DIF -> buf; inverse: buf -> DIT ->
 // scaled residues.
-template <int P, int LGR, int LGC, bool STAGED = false>
-__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct,
+// LCT >= 0: the tile width is the compile-time col_lct (smem offsets fold into
+// immediates: the radix-32 pass's 32 loads were ~5 instructions each with a
+// runtime width); -1: runtime lct_in.
+template <int P, int LGR, int LGC, bool STAGED = false, int LCT = -1>
+__device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTables& tab, int lct_in,
                                              int b, int op, int tile,
                                              const uint2* stage = nullptr,
                                              const uint2* s_tw = nullptr) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
   constexpr int lgC = LGC;
   const long long L = job.L;
@@ -558,11 +564,13 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
   }
 }
 
-template <int P, int LGR, int LGC>
-__device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab, int lct) {
+template <int P, int LGR, int LGC, int LCT = -1>
+__device__ __forceinline__ void col_inv_body(const ConvJob& job, const PlanTables& tab,
+                                             int lct_in) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGR);
   constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
+  const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
   const int b = blockIdx.y;  // grid (C / CT, batch, prime)
   constexpr int lgC = LGC;
@@ -949,9 +957,11 @@ __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, i
 }
 
 template <int LGR, int LGC>
-__global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct) {
-  const FwdIdx ix = fwd_idx(job, lct);
-#define PAB_B(P_) col_fwd_body<P_, LGR, LGC>(job, tab, lct, ix.b, ix.op, ix.tile);
+__global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct_in) {
+  constexpr int LCT = col_lct(LGR, LGC);
+  if (lct_in != LCT) __trap();  // the launcher's width is this constant
+  const FwdIdx ix = fwd_idx(job, LCT);
+#define PAB_B(P_) col_fwd_body<P_, LGR, LGC, false, LCT>(job, tab, LCT, ix.b, ix.op, ix.tile);
   PAB_PRIME_SWITCH(PAB_B, ix.prime)
 #undef PAB_B
 }
@@ -960,9 +970,11 @@ __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab,
 // tile fastest, then operand, then block.  Dynamic smem: the transform panel
 // plus the stage (rows x CT x 8 bytes).
 template <int LGR, int LGC>
-__global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab, int lct) {
+__global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab, int lct_in) {
   extern __shared__ u32 smem[];
-  const int CT = 1 << lct;
+  constexpr int lct = col_lct(LGR, LGC);
+  if (lct_in != lct) __trap();  // the launcher's width is this constant
+  constexpr int CT = 1 << lct;
   const unsigned tc = 1u << (LGC - lct);
   const int tile = (int)(blockIdx.x % tc);
   const int rest = (int)(blockIdx.x / tc);
@@ -977,11 +989,11 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
   uint2* s_tw = stage + (rows << lct);
   for (int i = threadIdx.x; i < job.np * NTW; i += blockDim.x)
     s_tw[i] = __ldg(tab.stw + ((i / NTW) * 2) * kTwN + (i % NTW));
-  stage_operand(ov, stage, rows, lct, LGC, tile << lct);  // (its barrier covers s_tw too)
+  stage_operand<lct>(ov, stage, rows, lct, LGC, tile << lct);  // (its barrier covers s_tw too)
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
     if (P >= job.p0 && P < job.p0 + job.pn) {
-      col_fwd_body<P, LGR, LGC, true>(job, tab, lct, b, op, tile, stage, s_tw + P * NTW);
+      col_fwd_body<P, LGR, LGC, true, lct>(job, tab, lct, b, op, tile, stage, s_tw + P * NTW);
       __syncthreads();  // the next prime reuses the transform panel
     }
   });
@@ -1014,8 +1026,10 @@ __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int 
 }
 
 template <int LGR, int LGC>
-__global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct) {
-#define PAB_B(P_) col_inv_body<P_, LGR, LGC>(job, tab, lct);
+__global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct_in) {
+  constexpr int LCT = col_inv_lct(LGR, LGC);
+  if (lct_in != LCT) __trap();  // the launcher's width is this constant
+#define PAB_B(P_) col_inv_body<P_, LGR, LGC, LCT>(job, tab, LCT);
   PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
 }

@@ -860,22 +860,6 @@ static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
   return nullptr;
 }
 
-static int col_lct(int lgR, int lgC) {
-  int lct = 14 - lgR;  // ~16K words per CTA
-  if (lct > 5) lct = 5;
-  if (lct < 13 - lgR) lct = 13 - lgR;  // the radix-32 pass has >= 256 tasks (one per thread)
-  if (lct < 3) lct = 3;
-  if (lct > lgC) lct = lgC;
-  return lct;
-}
-
-static int col_lct_rows(long long R, int lgC) {  // ~16K words (R rows x CT columns) per CTA
-  int lct = 5;
-  while (lct > 3 && (R << lct) > 16384) --lct;
-  if (lct > lgC) lct = lgC;
-  return lct;
-}
-
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
   if (job.m == 1 && job.lgR == 0) {
@@ -947,8 +931,8 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     prof::Scope ps_("k_col_inv", st);
     // pow2 inverse: half-width tiles in 128-thread CTAs while >= 32 columns wide
     // (same resident warps, more independent CTAs; measured -1.5%)
-    const int xi = job.m == 1 && lct >= 6 ? 1 : 0;
-    const int lci = lct - xi;
+    const int lci = job.m == 1 ? col_inv_lct(job.lgR, job.lgC) : lct;
+    const int xi = lct - lci;
     const size_t smi = (size_t)job.m * sm_len(job.lgR) * (1u << lci) * 4;
     ci<<<dim3(1u << (job.lgC - lci), job.batch, job.pn), ct_threads >> xi, smi, st>>>(job, tab,
                                                                                    lci);

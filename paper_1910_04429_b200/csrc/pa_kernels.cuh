@@ -57,6 +57,27 @@ struct ConvJob {
   int fwd_chunk;               // forward column pass: blocks per L2-resident chunk (grid order)
 };
 
+// Column-pass tile widths (columns per CTA, log2), shared by the launcher and the
+// kernels so the kernels can take them as compile-time constants.
+__host__ __device__ constexpr int col_lct(int lgR, int lgC) {
+  int lct = 14 - lgR;  // ~16K words per CTA
+  if (lct > 5) lct = 5;
+  if (lct < 13 - lgR) lct = 13 - lgR;  // the radix-32 pass has >= 256 tasks (one per thread)
+  if (lct < 3) lct = 3;
+  if (lct > lgC) lct = lgC;
+  return lct;
+}
+// pow2 inverse: half-width tiles in 128-thread CTAs while >= 32 columns wide
+__host__ __device__ constexpr int col_inv_lct(int lgR, int lgC) {
+  return col_lct(lgR, lgC) - (col_lct(lgR, lgC) >= 6 ? 1 : 0);
+}
+__host__ __device__ constexpr int col_lct_rows(long long R, int lgC) {  // ~16K words per CTA
+  int lct = 5;
+  while (lct > 3 && (R << lct) > 16384) --lct;
+  if (lct > lgC) lct = lgC;
+  return lct;
+}
+
 constexpr int kCarryWarps = 8;                           // warps per carry CTA
 constexpr int kCarryRows = 8;                            // 32-word rows per warp
 constexpr int kCarryThreads = 32 * kCarryWarps;
