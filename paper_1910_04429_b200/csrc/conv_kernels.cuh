@@ -943,14 +943,18 @@ template <int M, int LGR2, int LGC>
 #ifndef PAB_COLM3_FWD_REGS
 #define PAB_COLM3_FWD_REGS 64
 #endif
-__global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob job, PlanTables tab, int lct) {
+__global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob job, PlanTables tab, int lct_in) {
+  constexpr int lct = col_lct_rows((long long)M << LGR2, LGC);  // compile-time tile width
+  if (lct_in != lct) __trap();
   const FwdIdx ix = fwd_idx(job, lct);
 #define PAB_B(P_) colm_fwd_body<P_, M, LGR2, LGC>(job, tab, lct, ix.b, ix.op, ix.tile);
   PAB_PRIME_SWITCH(PAB_B, ix.prime)
 #undef PAB_B
 }
 template <int M, int LGR2, int LGC>
-__global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct) {
+__global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct_in) {
+  constexpr int lct = col_lct_rows((long long)M << LGR2, LGC);  // compile-time tile width
+  if (lct_in != lct) __trap();
 #define PAB_B(P_) colm_inv_body<P_, M, LGR2, LGC>(job, tab, lct);
   PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
@@ -1003,9 +1007,13 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
 // coefficients (row < ceil(kc / C)) once, then each prime's radix-M + pow2
 // column DFT reads them from smem.
 template <int M, int LGR2, int LGC>
-__global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int lct) {
+__global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int lct_in) {
   extern __shared__ u32 smem[];
-  const int CT = 1 << lct;
+  // half-width tiles (the launcher's lcta), compile-time
+  constexpr int lct = col_lct_rows((long long)M << LGR2, LGC) - 1 < 2
+                          ? 2 : col_lct_rows((long long)M << LGR2, LGC) - 1;
+  if (lct_in != lct) __trap();
+  constexpr int CT = 1 << lct;
   const unsigned tc = 1u << (LGC - lct);
   const int tile = (int)(blockIdx.x % tc);
   const int rest = (int)(blockIdx.x / tc);
