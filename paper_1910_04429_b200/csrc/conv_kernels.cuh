@@ -8,7 +8,7 @@ namespace pab {
 
 typedef void (*ConvKernel)(ConvJob, PlanTables, int);
 struct ConvKernels {
-  ConvKernel row, row_small;
+  ConvKernel row, row_small, row_tw4;
   ConvKernel col_fwd, col_inv;      // column passes with lgC == LG (lg even)
   ConvKernel col_fwd1, col_inv1;    // column passes with lgC == LG + 1 (lg odd)
   ConvKernel col_fwd_all, col_fwd_all1;  // all-primes forward column pass (lgC == LG, LG + 1)
@@ -207,7 +207,11 @@ __device__ __forceinline__ u32 row_k1(int q, int m, int lgR) {
 // c-rows (A) then the NR x-rows (X), each sm_len(LGC) words.
 // SMALL (lgR == 0): the row is the whole transform; read the operand words,
 // write scaled residues.
-template <int P, int LGC, bool SMALL>
+// TW4: the four-step twiddles come from the precomputed tables (tab.tw4) only;
+// otherwise either path, chosen by tab.tw4 at run time.  The table-only variant
+// keeps the generated path's code out of the instruction stream (k_row<12> is
+// ~3.7K instructions per prime).
+template <int P, int LGC, bool SMALL, bool TW4 = false>
 __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& tab, int lnr) {
   extern __shared__ u32 smem[];
   constexpr PassPlan PP = pass_plan(LGC);
@@ -250,7 +254,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
           v[0][k] = ra[k << SLO0];
           v[1][k] = rx[k << SLO0];
         }
-        if (tab.tw4) {  // precomputed Shoup twiddles (coalesced, L2-resident)
+        if (TW4 || tab.tw4) {  // precomputed Shoup twiddles (coalesced, L2-resident)
           const uint2* tp = tab.tw4 + (long long)(P * 2 + 0) * L + ((long long)q << LGC) + o;
 #pragma unroll
           for (int k = 0; k < (1 << RS0); ++k) {
@@ -423,7 +427,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
         }
       } else {
         u32* rx = gX + ((long long)q << LGC) + o;
-        if (tab.tw4) {
+        if (TW4 || tab.tw4) {
           const uint2* tp = tab.tw4 + (long long)(P * 2 + 1) * L + ((long long)q << LGC) + o;
 #pragma unroll
           for (int k = 0; k < (1 << RS0); ++k)
@@ -443,9 +447,9 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
   }
 }
 
-template <int LGC, bool SMALL>
+template <int LGC, bool SMALL, bool TW4 = false>
 __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
-#define PAB_B(P_) row_body<P_, LGC, SMALL>(job, tab, lnr);
+#define PAB_B(P_) row_body<P_, LGC, SMALL, TW4>(job, tab, lnr);
   PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
 }
@@ -1067,6 +1071,9 @@ ConvKernels make_conv_kernels() {
   ConvKernels k{};
   k.row = k_row<LG, false>;
   k.row_small = k_row<LG, true>;
+  // table-only variant where the generated path's code costs i-cache (lgC = 12:
+  // k_row -2%); at lgC <= 11 ptxas schedules it in fewer registers and it loses 1-3%
+  if constexpr (LG == 12) k.row_tw4 = k_row<LG, false, true>;
   if constexpr (LG >= 6) {
     k.col_inv = k_col_inv<LG, LG>;
     if constexpr (LG <= 8) {

@@ -924,8 +924,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
   {
     prof::Scope ps_("k_row", st);
-    row_kernel(job.lgC, false)<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), 128, smr,
-                                 st>>>(job, tab, lnr);
+    const ConvKernel rt = tab.tw4 ? conv_for(job.lgC).row_tw4 : nullptr;
+    const ConvKernel rk = rt ? rt : row_kernel(job.lgC, false);
+    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), 128, smr, st>>>(job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
