@@ -895,30 +895,42 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
   if constexpr (FUSE) {
     // top pow2 DIT stages of the M sub-columns fused with the inverse radix-M stage
     constexpr int RS0 = PP.rs[0], SLO0 = PP.slo[0];
-    for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
-      const int t = task & (CT - 1), o = task >> lct;
-      u32 v[M][1 << RS0];
-#pragma unroll
-      for (int s = 0; s < M; ++s) {
-#pragma unroll
-        for (int k = 0; k < (1 << RS0); ++k)
-          v[s][k] = smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t];
-        dit_rt<P, RS0, SLO0>(v[s], twi + o);
-      }
-#pragma unroll
-      for (int k = 0; k < (1 << RS0); ++k) {
-        const int j = o + (k << SLO0);
-        u32 a[M];
-        a[0] = red(v[0][k], PK<P>::two_p);
-#pragma unroll
-        for (int s = 1; s < M; ++s) a[s] = shoup(v[s][k], __ldg(trad + j * s), PK<P>::p);
-        radix_m<P, M, true>(a);
+    // HALF (nres <= L/2, always for the hash): rows >= R/2 are never stored, which
+    // is sub-columns s > M/2, and s = M/2 for j >= R2/2 (k >= NK/2) -- compile-time
+    // per (s, k), so their outputs and radix-M arithmetic fold away
+    auto pass = [&](auto half_c) {
+      constexpr bool HALF = decltype(half_c)::value;
+      for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+        const int t = task & (CT - 1), o = task >> lct;
+        u32 v[M][1 << RS0];
 #pragma unroll
         for (int s = 0; s < M; ++s) {
-          const int gi = ((j + s * R2) << lgC) + c0 + t;
-          if (gi < nres) res[gi] = red(a[s], PK<P>::p);  // [0, 2p) -> canonical; scale in the twiddles
+#pragma unroll
+          for (int k = 0; k < (1 << RS0); ++k)
+            v[s][k] = smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t];
+          dit_rt<P, RS0, SLO0>(v[s], twi + o);
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << RS0); ++k) {
+          const int j = o + (k << SLO0);
+          u32 a[M];
+          a[0] = red(v[0][k], PK<P>::two_p);
+#pragma unroll
+          for (int s = 1; s < M; ++s) a[s] = shoup(v[s][k], __ldg(trad + j * s), PK<P>::p);
+          radix_m<P, M, true>(a);
+#pragma unroll
+          for (int s = 0; s < M; ++s) {
+            if (HALF && !(s < M / 2 || (s == M / 2 && k < (1 << RS0) / 2))) continue;
+            const int gi = ((j + s * R2) << lgC) + c0 + t;
+            if (gi < nres) res[gi] = red(a[s], PK<P>::p);  // [0, 2p) -> canonical; scale in the twiddles
+          }
         }
       }
+    };
+    if (job.nRes <= (L >> 1)) {
+      pass(std::integral_constant<bool, true>{});
+    } else {
+      pass(std::integral_constant<bool, false>{});
     }
     return;
   }
