@@ -683,6 +683,289 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry_lb(ConvJob job) {
   carry_tile<true, CW>(job, sm, b, (int)sm.tile, 0u);
 }
 
+// ---------------------------------------------------------------------------
+// Wide carry (cw = 2): lane-contiguous coefficient ranges.  Lane l of a warp
+// CRTs 8 consecutive coefficients and owns the words of coefficient positions
+// cb + 2 .. cb + 9 (cb = its first CRT): their column sums need x_c, x_{c-1},
+// x_{c-2}, all in the lane or its upper neighbour (6 shuffles), and its 16
+// words resolve with a sequential carry chain in registers.  A warp owns 254
+// positions (508 words; lane 31 owns 6) from 256 CRTs, so warps need no
+// neighbour CRTs.  Carries cross lanes by a 5-step shuffle scan of carry
+// functions c -> q + (c >= t), warps and tiles compose them as in carry_tile
+// (decoupled look-back), and each warp stages its words in smem to write the
+// shifted key coalesced.  Replaces the warp-striped layout's per-word routing
+// shuffles and ballots (~325 -> ~150 instructions per coefficient).
+constexpr int kWPos = 32 * 8 - 2;                      // positions a warp owns
+constexpr int kWWords = 2 * kWPos;                     // 508 words per warp
+constexpr int kWTileWords = kCarryWarps * kWWords;     // 4064 words per tile
+constexpr int kWStage = 17 * 32;                       // per-warp staging, 17-word lane stride
+
+struct WideSmem {
+  u32 tile, cin;
+  volatile u32 cin_ready;
+  u32 wq[kCarryWarps], wt[kCarryWarps];
+  u32 first[kCarryWarps];  // each warp's first word, resolved with carry-in 0
+  u32 stage[kCarryWarps][kWStage];
+};
+
+__device__ __forceinline__ u32 res_or0(const u32* __restrict__ res, long long L, int i,
+                                       long long k, long long nres) {
+  return (k >= 0 && k < nres) ? __ldg(res + i * L + k) : 0u;
+}
+
+#ifndef PAB_WIDE_MINB
+#define PAB_WIDE_MINB 3
+#endif
+__global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob job) {
+  __shared__ WideSmem sm;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
+  __syncthreads();
+  const int tile = (int)sm.tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool last = warp == kCarryWarps - 1;
+  const long long L = job.L, nres = job.nRes, nT = job.nT;
+  const u32* res = job.buf + (long long)b * 2 * job.np * L;  // prime i at res + i * L
+  const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
+  const long long kd = dw ? job.kD : 0;
+  const long long ps = (long long)tile * (kCarryWarps * kWPos) + (long long)warp * kWPos;
+  const long long cb = ps - 2 + 8 * lane;  // first CRT coefficient of this lane
+  const long long wb = 2 * ps;             // first word of this warp
+  const long long lw = wb + 16 * lane;     // first word of this lane
+  const int nwl = lane == 31 ? 12 : 16;    // words this lane owns
+
+  // residues -> CRT of coefficients cb .. cb + 7
+  u32 X[8][5];
+  if (cb >= 0 && cb + 8 <= nres) {  // cb is even and L a multiple of 2: 8-byte pairs
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const uint2* rp = reinterpret_cast<const uint2*>(res + i * L + cb);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint2 v = __ldg(rp + j);
+        X[2 * j][i] = v.x;
+        X[2 * j + 1][i] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) X[j][i] = res_or0(res, L, i, cb + j, nres);
+  }
+  // the last warp also needs x_P, P = the next tile's first position (lane 31)
+  u32 XP[5] = {0u, 0u, 0u, 0u, 0u};
+  const long long P = ps + kWPos;
+  if (last && lane == 31 && P < nres) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) XP[i] = __ldg(res + i * L + P);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) crt5(X[j], X[j]);
+  if (last && lane == 31 && P < nres) crt5(XP, XP);
+  // D words of this lane (loaded after the CRT: fewer live registers)
+  u32 DV[16];
+  if (lw + 16 <= kd && (reinterpret_cast<uintptr_t>(dw + lw) & 7) == 0) {
+    const uint2* dp = reinterpret_cast<const uint2*>(dw + lw);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint2 v = __ldg(dp + w);
+      DV[2 * w] = v.x;
+      DV[2 * w + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < 16; ++w) DV[w] = fetch_word(dw, lw + w, kd, job.maskD);
+  }
+  // x_{cb+8}[0..3] and x_{cb+9}[0..1] from lane + 1 (its first two coefficients)
+  u32 N8[4], N9[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) N8[i] = __shfl_down_sync(0xFFFFFFFFu, X[0][i], 1);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) N9[i] = __shfl_down_sync(0xFFFFFFFFu, X[1][i], 1);
+  // column sums of positions c = cb + 2 + q (q < 8): words 2q, 2q + 1 of the lane
+  u32 W[16];
+  u32 cq = 0;  // carry out of the lane with carry-in 0
+  {
+    u64 carry = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = q + 2;  // x_c = X[j] (j < 8), N8 (j = 8), N9 (j = 9)
+      const u32 c0 = j < 8 ? X[j][0] : (j == 8 ? N8[0] : N9[0]);
+      const u32 c1 = j < 8 ? X[j][1] : (j == 8 ? N8[1] : N9[1]);
+      const u32 m2 = j - 1 < 8 ? X[j - 1][2] : N8[2];
+      const u32 m3 = j - 1 < 8 ? X[j - 1][3] : N8[3];
+      const u32 m4 = X[j - 2][4];
+      const bool own = lane != 31 || q < 6;
+      const u64 se = own ? (u64)c0 + m2 + m4 + DV[2 * q] + carry : 0ull;
+      W[2 * q] = (u32)se;
+      const u64 so = own ? (u64)c1 + m3 + DV[2 * q + 1] + (se >> 32) : 0ull;
+      W[2 * q + 1] = (u32)so;
+      carry = own ? (so >> 32) : carry;
+    }
+    cq = (u32)carry;
+  }
+  // lane carry function c -> cq + (c >= t): the extra carry needs word 0 + c to
+  // overflow and every other owned word to be all-ones
+  u32 tq;
+  {
+    bool ones = true;
+#pragma unroll
+    for (int w = 1; w < 16; ++w) ones &= (w >= nwl) || W[w] == 0xFFFFFFFFu;
+    tq = (ones && W[0] != 0u) ? (0u - W[0]) : kInf;
+  }
+  // warp inclusive scan of the lane functions (lower lanes applied first)
+  CarryFn inc{cq, tq, false};
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const CarryFn g{__shfl_up_sync(0xFFFFFFFFu, inc.q, d), __shfl_up_sync(0xFFFFFFFFu, inc.t, d),
+                    false};
+    if (lane >= d) inc = cf_compose(inc, g);
+  }
+  CarryFn exl{__shfl_up_sync(0xFFFFFFFFu, inc.q, 1), __shfl_up_sync(0xFFFFFFFFu, inc.t, 1), lane == 0};
+  const CarryFn f{__shfl_sync(0xFFFFFFFFu, inc.q, 31), __shfl_sync(0xFFFFFFFFu, inc.t, 31), false};
+  if (lane == 0) {
+    sm.wq[warp] = f.q;
+    sm.wt[warp] = f.t;
+    sm.first[warp] = W[0];
+    if (warp == 0) sm.cin_ready = 0u;
+  }
+  __syncthreads();
+  CarryFn wpre{0, 0, true}, agg{0, 0, true};
+#pragma unroll
+  for (int w = 0; w < kCarryWarps; ++w) {
+    const CarryFn fw{sm.wq[w], sm.wt[w], false};
+    if (w < warp) wpre = cf_compose(fw, wpre);
+    agg = cf_compose(fw, agg);
+  }
+  // carry into the tile (decoupled look-back by warp 0; other warps wait only
+  // if their predecessors in the tile let a carry through)
+  u32 tile_cin = 0;
+  if (warp == 0) {
+    volatile unsigned long long* st = job.tile_state + (long long)b * job.tiles;
+    u32 cin = 0;
+    if (tile > 0) {
+      if (lane == 0) st[tile] = (1ull << 62) | ((unsigned long long)agg.q << 32) | agg.t;
+      CarryFn F{0, 0, true};
+      int base = tile - 1;
+      while (true) {
+        const int j = base - lane;
+        const unsigned long long v = j >= 0 ? st[j] : (2ull << 62);
+        const u32 flag = (u32)(v >> 62);
+        const unsigned zero = __ballot_sync(0xFFFFFFFFu, flag == 0);
+        const unsigned pre = __ballot_sync(0xFFFFFFFFu, flag == 2);
+        const int first = pre ? __ffs(pre) - 1 : 32;
+        const unsigned need = first == 32 ? 0xFFFFFFFFu : ((2u << first) - 1u);
+        if (zero & need) continue;
+        const u32 q = (u32)((v >> 32) & 0xFFu), t = (u32)v;
+        for (int i = 0; i < first; ++i) {
+          const CarryFn g{__shfl_sync(0xFFFFFFFFu, q, i), __shfl_sync(0xFFFFFFFFu, t, i), false};
+          F = cf_compose(F, g);
+        }
+        if (first < 32) {
+          cin = cf_apply(F, __shfl_sync(0xFFFFFFFFu, q, first));
+          break;
+        }
+        base -= 32;
+      }
+    }
+    if (lane == 0) {
+      st[tile] = (2ull << 62) | ((unsigned long long)cf_apply(agg, cin) << 32);
+      sm.cin = cin;
+      __threadfence_block();
+      sm.cin_ready = 1u;
+    }
+    tile_cin = cin;
+  } else if (wpre.t != kInf) {
+    while (sm.cin_ready == 0u) {
+    }
+    __threadfence_block();
+    tile_cin = *((volatile u32*)&sm.cin);
+  }
+  const u32 cin_w = cf_apply(wpre, tile_cin);
+  const u32 cw_out = cf_apply(f, cin_w);    // carry out of the warp
+  const u32 cl = cf_apply(exl, cin_w);      // carry into this lane
+  // add it at word 0 and ripple through all-ones words (almost always stops at once)
+  W[0] += cl;
+  if (W[0] < cl) {
+    u32 cr = 1u;
+#pragma unroll
+    for (int w = 1; w < 16; ++w) {
+      if (w < nwl && cr) {
+        W[w] += 1u;
+        cr = W[w] == 0u ? 1u : 0u;
+      }
+    }
+  }
+  // clear words >= n_mod_bits
+  const long long rbits = job.n_mod_bits - 32ll * (nT - 1);
+  const u32 tmask = rbits >= 32 ? 0xFFFFFFFFu : ((1u << rbits) - 1u);
+  if (wb + kWWords >= nT) {
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+      const long long g = lw + w;
+      W[w] = g >= nT ? 0u : (g == nT - 1 ? (W[w] & tmask) : W[w]);
+    }
+  }
+  // the word after the warp: the next warp's first word + this warp's carry out,
+  // or (last warp) the next tile's first word
+  u32 nextw;
+  {
+    const long long k = wb + kWWords;
+    if (last) {
+      const u32 x1 = __shfl_sync(0xFFFFFFFFu, X[7][2], 31);  // x_{P-1}[2]
+      const u32 x2 = __shfl_sync(0xFFFFFFFFu, X[6][4], 31);  // x_{P-2}[4]
+      const u32 x0 = __shfl_sync(0xFFFFFFFFu, XP[0], 31);
+      nextw = x0 + x1 + x2 + fetch_word(dw, k, kd, job.maskD) + cw_out;
+    } else {
+      nextw = sm.first[warp + 1] + cw_out;
+    }
+    nextw = k >= nT ? 0u : (k == nT - 1 ? (nextw & tmask) : nextw);
+  }
+  // stage the warp's words, then write the shifted key coalesced
+  u32* sg = sm.stage[warp];
+#pragma unroll
+  for (int w = 0; w < 16; ++w)
+    if (w < nwl) sg[17 * lane + w] = W[w];
+  __syncwarp();
+  const long long ws = job.shift >> 5;
+  const int sh = (int)(job.shift & 31);
+  uint8_t* outb = job.out_words ? nullptr : job.out_bytes + (long long)b * job.out_stride;
+  u32* outw = job.out_words ? job.out_words + (long long)b * job.mw : nullptr;
+  const long long o0 = wb - ws;  // output word of the warp's first word
+  if (o0 >= 0 && o0 + kWWords <= job.mw && (outw || 4 * (o0 + kWWords) <= job.rbytes)) {
+    // the whole warp inside the key: no bounds, whole words
+    u32* ow = outw ? outw : reinterpret_cast<u32*>(outb);
+    if (sh == 0) {
+#pragma unroll 4
+      for (int j = lane; j < kWWords; j += 32) ow[o0 + j] = sg[17 * (j >> 4) + (j & 15)];
+    } else {
+#pragma unroll 4
+      for (int j = lane; j < kWWords; j += 32) {
+        const u32 lo = sg[17 * (j >> 4) + (j & 15)];
+        const u32 hi = j + 1 < kWWords ? sg[17 * ((j + 1) >> 4) + ((j + 1) & 15)] : nextw;
+        ow[o0 + j] = (lo >> sh) | (hi << (32 - sh));
+      }
+    }
+    return;
+  }
+#pragma unroll 4
+  for (int j = lane; j < kWWords; j += 32) {
+    const long long oj = o0 + j;
+    if (oj < 0 || oj >= job.mw) continue;
+    const u32 lo = sg[17 * (j >> 4) + (j & 15)];
+    const u32 hi = j + 1 < kWWords ? sg[17 * ((j + 1) >> 4) + ((j + 1) & 15)] : nextw;
+    const u32 y = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
+    if (outw) {
+      outw[oj] = y;
+    } else if (4 * oj + 4 <= job.rbytes) {
+      reinterpret_cast<u32*>(outb)[oj] = y;
+    } else {
+      for (int q = 0; q < 4 && 4 * oj + q < job.rbytes; ++q) outb[4 * oj + q] = (uint8_t)(y >> (8 * q));
+    }
+  }
+}
+
 // One CTA per block walking its tiles in order (many blocks): no inter-CTA waits.
 template <int CW>
 __global__ void __launch_bounds__(kCarryThreads) k_carry_seq(ConvJob job) {
@@ -950,14 +1233,20 @@ bool conv_supported(int m, int lgR, int lgC) {
 
 void launch_carry(const ConvJob& job, cudaStream_t st) {
   prof::Scope ps_("k_carry", st);
-  static const int force = [] {  // development override: PAB_CARRY_MODE=seq|lb
+  static const int force = [] {  // development override: PAB_CARRY_MODE=seq|lb|wide
     const char* e = getenv("PAB_CARRY_MODE");
-    return e ? (e[0] == 's' ? 1 : 2) : 0;
+    return e ? (e[0] == 's' ? 1 : e[0] == 'l' ? 2 : 0) : 0;
   }();
   // look-back everywhere (batch-major grid, measured faster than one CTA per
   // block walking its tiles even at 1024 blocks); sequential for one-tile blocks
   const bool seq = job.tiles == 1 || force == 1;
   const dim3 grid = seq ? dim3(1, job.batch) : dim3(job.batch, job.tiles);
+  if (job.cw == 2 && force != 1 && force != 2) {  // wide layout (PAB_CARRY_MODE=seq|lb: the old ones)
+    ConvJob jw = job;
+    jw.tiles = (int)((job.nT + kWTileWords - 1) / kWTileWords);  // <= job.tiles: state fits
+    k_carry_wide<<<dim3(job.batch, jw.tiles), kCarryThreads, 0, st>>>(jw);
+    return;
+  }
   if (job.cw == 2) {
     if (seq) k_carry_seq<2><<<grid, kCarryThreads, 0, st>>>(job);
     else k_carry_lb<2><<<grid, kCarryThreads, 0, st>>>(job);

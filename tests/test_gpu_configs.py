@@ -226,9 +226,12 @@ def test_exhaustive_alpha6_on_gpu_batched():
         assert np.array_equal(out, want.reshape(-1).astype(np.uint8))
 
 
-def test_sequential_carry_mode_matches_oracle():
-    # the one-CTA-per-block carry (production only for one-tile blocks) across
-    # many tiles, forced through its development switch in a fresh process
+@pytest.mark.parametrize("mode", ["seq", "lb"])
+def test_alternate_carry_modes_match_oracle(mode):
+    # the warp-striped carries (production only for 32-bit coefficients; with
+    # 64-bit coefficients the lane-contiguous k_carry_wide runs): one CTA per
+    # block walking its tiles (seq) or the decoupled look-back (lb), forced
+    # through their development switch in a fresh process
     import os
     import subprocess
     import sys
@@ -253,7 +256,7 @@ for cw in (2, 1):
             assert out[i].tobytes() == want, (cw, n, i)
 print("SEQ_OK")
 """
-    env = dict(os.environ, PAB_CARRY_MODE="seq")
+    env = dict(os.environ, PAB_CARRY_MODE=mode)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
