@@ -695,10 +695,17 @@ __global__ void __launch_bounds__(kCarryThreads) k_carry_lb(ConvJob job) {
 // (decoupled look-back), and each warp stages its words in smem to write the
 // shifted key coalesced.  Replaces the warp-striped layout's per-word routing
 // shuffles and ballots (~325 -> ~150 instructions per coefficient).
-constexpr int kWPos = 32 * 8 - 2;                      // positions a warp owns
+#ifndef PAB_WIDE_CPT
+#define PAB_WIDE_CPT 8
+#endif
+constexpr int kWCpt = PAB_WIDE_CPT;                    // CRTs (positions) per lane
+constexpr int kWLw = 2 * kWCpt;                        // words per lane
+constexpr int kWPos = 32 * kWCpt - 2;                  // positions a warp owns
 constexpr int kWWords = 2 * kWPos;                     // 508 words per warp
 constexpr int kWTileWords = kCarryWarps * kWWords;     // 4064 words per tile
-constexpr int kWStage = 17 * 32;                       // per-warp staging, 17-word lane stride
+constexpr int kWStage = (kWLw + 1) * 32;              // per-warp staging, padded lane stride
+static_assert(kWTileWords >= kCarryTile, "look-back state is sized for kCarryTile tiles");
+// (4 coefficients per lane: 64 registers and no spills, but 0.181 vs 0.172 ms at C2)
 
 struct WideSmem {
   u32 tile, cin;
@@ -729,19 +736,19 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
   const long long kd = dw ? job.kD : 0;
   const long long ps = (long long)tile * (kCarryWarps * kWPos) + (long long)warp * kWPos;
-  const long long cb = ps - 2 + 8 * lane;  // first CRT coefficient of this lane
+  const long long cb = ps - 2 + kWCpt * lane;  // first CRT coefficient of this lane
   const long long wb = 2 * ps;             // first word of this warp
-  const long long lw = wb + 16 * lane;     // first word of this lane
-  const int nwl = lane == 31 ? 12 : 16;    // words this lane owns
+  const long long lw = wb + kWLw * lane;     // first word of this lane
+  const int nwl = lane == 31 ? kWLw - 4 : kWLw;    // words this lane owns
 
   // residues -> CRT of coefficients cb .. cb + 7
-  u32 X[8][5];
-  if (cb >= 0 && cb + 8 <= nres) {  // cb is even and L a multiple of 2: 8-byte pairs
+  u32 X[kWCpt][5];
+  if (cb >= 0 && cb + kWCpt <= nres) {  // cb is even and L a multiple of 2: 8-byte pairs
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       const uint2* rp = reinterpret_cast<const uint2*>(res + i * L + cb);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kWCpt / 2; ++j) {
         const uint2 v = __ldg(rp + j);
         X[2 * j][i] = v.x;
         X[2 * j + 1][i] = v.y;
@@ -751,7 +758,7 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
 #pragma unroll
     for (int i = 0; i < 5; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) X[j][i] = res_or0(res, L, i, cb + j, nres);
+      for (int j = 0; j < kWCpt; ++j) X[j][i] = res_or0(res, L, i, cb + j, nres);
   }
   // the last warp also needs x_P, P = the next tile's first position (lane 31)
   u32 XP[5] = {0u, 0u, 0u, 0u, 0u};
@@ -761,21 +768,21 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
     for (int i = 0; i < 5; ++i) XP[i] = __ldg(res + i * L + P);
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) crt5(X[j], X[j]);
+  for (int j = 0; j < kWCpt; ++j) crt5(X[j], X[j]);
   if (last && lane == 31 && P < nres) crt5(XP, XP);
   // D words of this lane (loaded after the CRT: fewer live registers)
-  u32 DV[16];
-  if (lw + 16 <= kd && (reinterpret_cast<uintptr_t>(dw + lw) & 7) == 0) {
+  u32 DV[kWLw];
+  if (lw + kWLw <= kd && (reinterpret_cast<uintptr_t>(dw + lw) & 7) == 0) {
     const uint2* dp = reinterpret_cast<const uint2*>(dw + lw);
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < kWCpt; ++w) {
       const uint2 v = __ldg(dp + w);
       DV[2 * w] = v.x;
       DV[2 * w + 1] = v.y;
     }
   } else {
 #pragma unroll
-    for (int w = 0; w < 16; ++w) DV[w] = fetch_word(dw, lw + w, kd, job.maskD);
+    for (int w = 0; w < kWLw; ++w) DV[w] = fetch_word(dw, lw + w, kd, job.maskD);
   }
   // x_{cb+8}[0..3] and x_{cb+9}[0..1] from lane + 1 (its first two coefficients)
   u32 N8[4], N9[2];
@@ -784,19 +791,19 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
 #pragma unroll
   for (int i = 0; i < 2; ++i) N9[i] = __shfl_down_sync(0xFFFFFFFFu, X[1][i], 1);
   // column sums of positions c = cb + 2 + q (q < 8): words 2q, 2q + 1 of the lane
-  u32 W[16];
+  u32 W[kWLw];
   u32 cq = 0;  // carry out of the lane with carry-in 0
   {
     u64 carry = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < kWCpt; ++q) {
       const int j = q + 2;  // x_c = X[j] (j < 8), N8 (j = 8), N9 (j = 9)
-      const u32 c0 = j < 8 ? X[j][0] : (j == 8 ? N8[0] : N9[0]);
-      const u32 c1 = j < 8 ? X[j][1] : (j == 8 ? N8[1] : N9[1]);
-      const u32 m2 = j - 1 < 8 ? X[j - 1][2] : N8[2];
-      const u32 m3 = j - 1 < 8 ? X[j - 1][3] : N8[3];
+      const u32 c0 = j < kWCpt ? X[j][0] : (j == kWCpt ? N8[0] : N9[0]);
+      const u32 c1 = j < kWCpt ? X[j][1] : (j == kWCpt ? N8[1] : N9[1]);
+      const u32 m2 = j - 1 < kWCpt ? X[j - 1][2] : N8[2];
+      const u32 m3 = j - 1 < kWCpt ? X[j - 1][3] : N8[3];
       const u32 m4 = X[j - 2][4];
-      const bool own = lane != 31 || q < 6;
+      const bool own = lane != 31 || q < kWCpt - 2;
       const u64 se = own ? (u64)c0 + m2 + m4 + DV[2 * q] + carry : 0ull;
       W[2 * q] = (u32)se;
       const u64 so = own ? (u64)c1 + m3 + DV[2 * q + 1] + (se >> 32) : 0ull;
@@ -811,7 +818,7 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   {
     bool ones = true;
 #pragma unroll
-    for (int w = 1; w < 16; ++w) ones &= (w >= nwl) || W[w] == 0xFFFFFFFFu;
+    for (int w = 1; w < kWLw; ++w) ones &= (w >= nwl) || W[w] == 0xFFFFFFFFu;
     tq = (ones && W[0] != 0u) ? (0u - W[0]) : kInf;
   }
   // warp inclusive scan of the lane functions (lower lanes applied first)
@@ -890,7 +897,7 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   if (W[0] < cl) {
     u32 cr = 1u;
 #pragma unroll
-    for (int w = 1; w < 16; ++w) {
+    for (int w = 1; w < kWLw; ++w) {
       if (w < nwl && cr) {
         W[w] += 1u;
         cr = W[w] == 0u ? 1u : 0u;
@@ -902,7 +909,7 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   const u32 tmask = rbits >= 32 ? 0xFFFFFFFFu : ((1u << rbits) - 1u);
   if (wb + kWWords >= nT) {
 #pragma unroll
-    for (int w = 0; w < 16; ++w) {
+    for (int w = 0; w < kWLw; ++w) {
       const long long g = lw + w;
       W[w] = g >= nT ? 0u : (g == nT - 1 ? (W[w] & tmask) : W[w]);
     }
@@ -913,8 +920,8 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   {
     const long long k = wb + kWWords;
     if (last) {
-      const u32 x1 = __shfl_sync(0xFFFFFFFFu, X[7][2], 31);  // x_{P-1}[2]
-      const u32 x2 = __shfl_sync(0xFFFFFFFFu, X[6][4], 31);  // x_{P-2}[4]
+      const u32 x1 = __shfl_sync(0xFFFFFFFFu, X[kWCpt - 1][2], 31);  // x_{P-1}[2]
+      const u32 x2 = __shfl_sync(0xFFFFFFFFu, X[kWCpt - 2][4], 31);  // x_{P-2}[4]
       const u32 x0 = __shfl_sync(0xFFFFFFFFu, XP[0], 31);
       nextw = x0 + x1 + x2 + fetch_word(dw, k, kd, job.maskD) + cw_out;
     } else {
@@ -925,8 +932,8 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   // stage the warp's words, then write the shifted key coalesced
   u32* sg = sm.stage[warp];
 #pragma unroll
-  for (int w = 0; w < 16; ++w)
-    if (w < nwl) sg[17 * lane + w] = W[w];
+  for (int w = 0; w < kWLw; ++w)
+    if (w < nwl) sg[(kWLw + 1) * lane + w] = W[w];
   __syncwarp();
   const long long ws = job.shift >> 5;
   const int sh = (int)(job.shift & 31);
@@ -938,12 +945,12 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
     u32* ow = outw ? outw : reinterpret_cast<u32*>(outb);
     if (sh == 0) {
 #pragma unroll 4
-      for (int j = lane; j < kWWords; j += 32) ow[o0 + j] = sg[17 * (j >> 4) + (j & 15)];
+      for (int j = lane; j < kWWords; j += 32) ow[o0 + j] = sg[(kWLw + 1) * (j / kWLw) + (j % kWLw)];
     } else {
 #pragma unroll 4
       for (int j = lane; j < kWWords; j += 32) {
-        const u32 lo = sg[17 * (j >> 4) + (j & 15)];
-        const u32 hi = j + 1 < kWWords ? sg[17 * ((j + 1) >> 4) + ((j + 1) & 15)] : nextw;
+        const u32 lo = sg[(kWLw + 1) * (j / kWLw) + (j % kWLw)];
+        const u32 hi = j + 1 < kWWords ? sg[(kWLw + 1) * ((j + 1) / kWLw) + ((j + 1) % kWLw)] : nextw;
         ow[o0 + j] = (lo >> sh) | (hi << (32 - sh));
       }
     }
@@ -953,8 +960,8 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   for (int j = lane; j < kWWords; j += 32) {
     const long long oj = o0 + j;
     if (oj < 0 || oj >= job.mw) continue;
-    const u32 lo = sg[17 * (j >> 4) + (j & 15)];
-    const u32 hi = j + 1 < kWWords ? sg[17 * ((j + 1) >> 4) + ((j + 1) & 15)] : nextw;
+    const u32 lo = sg[(kWLw + 1) * (j / kWLw) + (j % kWLw)];
+    const u32 hi = j + 1 < kWWords ? sg[(kWLw + 1) * ((j + 1) / kWLw) + ((j + 1) % kWLw)] : nextw;
     const u32 y = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
     if (outw) {
       outw[oj] = y;
