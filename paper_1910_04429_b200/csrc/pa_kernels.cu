@@ -743,7 +743,21 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
 
   // residues -> CRT of coefficients cb .. cb + 7
   u32 X[kWCpt][5];
-  if (cb >= 0 && cb + kWCpt <= nres) {  // cb is even and L a multiple of 2: 8-byte pairs
+  if (cb >= 0 && cb + kWCpt <= nres && (cb & 3) == 0 && (L & 3) == 0) {
+    // 16-byte quads (cb mod 4 is warp-uniform: half the warps)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const uint4* rp = reinterpret_cast<const uint4*>(res + i * L + cb);
+#pragma unroll
+      for (int j = 0; j < kWCpt / 4; ++j) {
+        const uint4 v = __ldg(rp + j);
+        X[4 * j][i] = v.x;
+        X[4 * j + 1][i] = v.y;
+        X[4 * j + 2][i] = v.z;
+        X[4 * j + 3][i] = v.w;
+      }
+    }
+  } else if (cb >= 0 && cb + kWCpt <= nres) {  // cb is even and L a multiple of 2: 8-byte pairs
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       const uint2* rp = reinterpret_cast<const uint2*>(res + i * L + cb);
