@@ -442,7 +442,7 @@ Layout layout_for(u64 kmax, u64 L, u64 nT, u64 mw, u64 batch, int np) {
   Layout ly;
   ly.in_stride = round_up(kmax > 0 ? kmax : 1, 64);
   ly.L = L;
-  ly.tiles = ceil_div(nT, kCarryTile);
+  ly.tiles = ceil_div(nT, kCarryTileMin);  // look-back states for the smallest tile of any carry kernel
   ly.mw = mw;
   size_t off = 0;
   auto take = [&](size_t bytes) {

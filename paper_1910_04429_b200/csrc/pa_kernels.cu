@@ -702,17 +702,22 @@ constexpr int kWCpt = PAB_WIDE_CPT;                    // CRTs (positions) per l
 constexpr int kWLw = 2 * kWCpt;                        // words per lane
 constexpr int kWPos = 32 * kWCpt - 2;                  // positions a warp owns
 constexpr int kWWords = 2 * kWPos;                     // 508 words per warp
-constexpr int kWTileWords = kCarryWarps * kWWords;     // 4064 words per tile
+#ifndef PAB_WIDE_WARPS
+#define PAB_WIDE_WARPS 4
+#endif
+constexpr int kWWarps = PAB_WIDE_WARPS;                // warps per CTA (one tile)
+constexpr int kWThreads = 32 * kWWarps;
+constexpr int kWTileWords = kWWarps * kWWords;         // words per tile
 constexpr int kWStage = (kWLw + 1) * 32;              // per-warp staging, padded lane stride
-static_assert(kWTileWords >= kCarryTile, "look-back state is sized for kCarryTile tiles");
+static_assert(kWTileWords >= kCarryTileMin, "look-back state is sized for kCarryTileMin tiles");
 // (4 coefficients per lane: 64 registers and no spills, but 0.181 vs 0.172 ms at C2)
 
 struct WideSmem {
   u32 tile, cin;
   volatile u32 cin_ready;
-  u32 wq[kCarryWarps], wt[kCarryWarps];
-  u32 first[kCarryWarps];  // each warp's first word, resolved with carry-in 0
-  u32 stage[kCarryWarps][kWStage];
+  u32 wq[kWWarps], wt[kWWarps];
+  u32 first[kWWarps];  // each warp's first word, resolved with carry-in 0
+  u32 stage[kWWarps][kWStage];
 };
 
 __device__ __forceinline__ u32 res_or0(const u32* __restrict__ res, long long L, int i,
@@ -721,21 +726,21 @@ __device__ __forceinline__ u32 res_or0(const u32* __restrict__ res, long long L,
 }
 
 #ifndef PAB_WIDE_MINB
-#define PAB_WIDE_MINB 3
+#define PAB_WIDE_MINB 6
 #endif
-__global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob job) {
+__global__ void __launch_bounds__(kWThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob job) {
   __shared__ WideSmem sm;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
   __syncthreads();
   const int tile = (int)sm.tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool last = warp == kCarryWarps - 1;
+  const bool last = warp == kWWarps - 1;
   const long long L = job.L, nres = job.nRes, nT = job.nT;
   const u32* res = job.buf + (long long)b * 2 * job.np * L;  // prime i at res + i * L
   const u32* dw = job.srcD ? job.srcD + (long long)b * job.src_stride : nullptr;
   const long long kd = dw ? job.kD : 0;
-  const long long ps = (long long)tile * (kCarryWarps * kWPos) + (long long)warp * kWPos;
+  const long long ps = (long long)tile * (kWWarps * kWPos) + (long long)warp * kWPos;
   const long long cb = ps - 2 + kWCpt * lane;  // first CRT coefficient of this lane
   const long long wb = 2 * ps;             // first word of this warp
   const long long lw = wb + kWLw * lane;     // first word of this lane
@@ -854,7 +859,7 @@ __global__ void __launch_bounds__(kCarryThreads, PAB_WIDE_MINB) k_carry_wide(Con
   __syncthreads();
   CarryFn wpre{0, 0, true}, agg{0, 0, true};
 #pragma unroll
-  for (int w = 0; w < kCarryWarps; ++w) {
+  for (int w = 0; w < kWWarps; ++w) {
     const CarryFn fw{sm.wq[w], sm.wt[w], false};
     if (w < warp) wpre = cf_compose(fw, wpre);
     agg = cf_compose(fw, agg);
@@ -1258,22 +1263,26 @@ void launch_carry(const ConvJob& job, cudaStream_t st) {
     const char* e = getenv("PAB_CARRY_MODE");
     return e ? (e[0] == 's' ? 1 : e[0] == 'l' ? 2 : 0) : 0;
   }();
-  // look-back everywhere (batch-major grid, measured faster than one CTA per
-  // block walking its tiles even at 1024 blocks); sequential for one-tile blocks
-  const bool seq = job.tiles == 1 || force == 1;
-  const dim3 grid = seq ? dim3(1, job.batch) : dim3(job.batch, job.tiles);
+  // (the workspace holds look-back states for tiles of kCarryTileMin words;
+  // each kernel indexes them with its own tile count)
   if (job.cw == 2 && force != 1 && force != 2) {  // wide layout (PAB_CARRY_MODE=seq|lb: the old ones)
     ConvJob jw = job;
-    jw.tiles = (int)((job.nT + kWTileWords - 1) / kWTileWords);  // <= job.tiles: state fits
-    k_carry_wide<<<dim3(job.batch, jw.tiles), kCarryThreads, 0, st>>>(jw);
+    jw.tiles = (int)((job.nT + kWTileWords - 1) / kWTileWords);
+    k_carry_wide<<<dim3(job.batch, jw.tiles), kWThreads, 0, st>>>(jw);
     return;
   }
-  if (job.cw == 2) {
-    if (seq) k_carry_seq<2><<<grid, kCarryThreads, 0, st>>>(job);
-    else k_carry_lb<2><<<grid, kCarryThreads, 0, st>>>(job);
+  ConvJob jo = job;
+  jo.tiles = (int)((job.nT + kCarryTile - 1) / kCarryTile);
+  // look-back everywhere (batch-major grid, measured faster than one CTA per
+  // block walking its tiles even at 1024 blocks); sequential for one-tile blocks
+  const bool seq = jo.tiles == 1 || force == 1;
+  const dim3 grid = seq ? dim3(1, jo.batch) : dim3(jo.batch, jo.tiles);
+  if (jo.cw == 2) {
+    if (seq) k_carry_seq<2><<<grid, kCarryThreads, 0, st>>>(jo);
+    else k_carry_lb<2><<<grid, kCarryThreads, 0, st>>>(jo);
   } else {
-    if (seq) k_carry_seq<1><<<grid, kCarryThreads, 0, st>>>(job);
-    else k_carry_lb<1><<<grid, kCarryThreads, 0, st>>>(job);
+    if (seq) k_carry_seq<1><<<grid, kCarryThreads, 0, st>>>(jo);
+    else k_carry_lb<1><<<grid, kCarryThreads, 0, st>>>(jo);
   }
 }
 

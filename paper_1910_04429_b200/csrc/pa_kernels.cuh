@@ -82,6 +82,7 @@ constexpr int kCarryWarps = 8;                           // warps per carry CTA
 constexpr int kCarryRows = 8;                            // 32-word rows per warp
 constexpr int kCarryThreads = 32 * kCarryWarps;
 constexpr int kCarryTile = 32 * kCarryWarps * kCarryRows;  // words per tile
+constexpr int kCarryTileMin = 1000;  // smallest tile of any carry kernel (sizes the look-back state)
 
 constexpr int kTinyBits = 2048;  // single-warp schoolbook path (n <= kTinyBits)
 
