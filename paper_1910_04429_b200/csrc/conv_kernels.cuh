@@ -147,6 +147,16 @@ __device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, in
                                               int lgC, int c0) {
   const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
+  if (ov.cw == 2 && ((rows - 1) << lgC) + c0 + CT - 1 < ov.kc - 1) {
+    // every staged coefficient valid and unmasked (all but the operand's last tiles)
+    for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
+      const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
+      cp_async8(stage + e, ov.src + 2 * gi);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    return;
+  }
   for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
     const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
     if (gi < ov.kc - 1) {
