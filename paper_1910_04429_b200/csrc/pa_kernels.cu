@@ -1227,7 +1227,10 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   // rows: 4K words of rows (A+X: 8K words) per 128-thread CTA -- the same
   // resident warps as 256-thread CTAs of twice the rows (smem-bound), but
   // twice the independent CTAs per SM to overlap barriers (measured -4..6%)
-  int lnr = 12 - job.lgC;
+  // rows of up to 256 points: 8 rows per 64-thread CTA (C2 k_row -1%); longer
+  // rows: 4K words per 128-thread CTA (8 rows / 64 threads loses 1-2% at 2^9+)
+  const bool narrow = job.lgC <= 8;
+  int lnr = 12 - job.lgC - (narrow ? 1 : 0);
   if (lnr < 0) lnr = 0;
   if (lnr > job.lgR) lnr = job.lgR;
   const size_t smr = (size_t)sm_len(job.lgC) * (2u << lnr) * 4;
@@ -1235,7 +1238,8 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     prof::Scope ps_("k_row", st);
     const ConvKernel rt = tab.tw4 ? conv_for(job.lgC).row_tw4 : nullptr;
     const ConvKernel rk = rt ? rt : row_kernel(job.lgC, false);
-    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), 128, smr, st>>>(job, tab, lnr);
+    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), narrow ? 64 : 128, smr, st>>>(job, tab,
+                                                                                      lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
