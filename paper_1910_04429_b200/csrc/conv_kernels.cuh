@@ -217,6 +217,9 @@ __device__ __forceinline__ u32 row_k1(int q, int m, int lgR) {
 // c-rows (A) then the NR x-rows (X), each sm_len(LGC) words.
 // SMALL (lgR == 0): the row is the whole transform; read the operand words,
 // write scaled residues.
+#ifndef PAB_ROW_REG2_MIN
+#define PAB_ROW_REG2_MIN 7  // last row pass keeps A and X in registers together above this lgC (C2 k_row -2%)
+#endif
 // TW4: the four-step twiddles come from the precomputed tables (tab.tw4) only;
 // otherwise either path, chosen by tab.tw4 at run time.  The table-only variant
 // keeps the generated path's code out of the instruction stream (k_row<12> is
@@ -363,7 +366,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
             m = shoup(m, gam, PK<P>::p);
           }
         }
-      } else if constexpr (LGC > 8) {
+      } else if constexpr (LGC > PAB_ROW_REG2_MIN) {
         const int base = row * T + sm_idx(g << RSL);
         u32 a[1][1 << RSL], x[1][1 << RSL];
 #pragma unroll
