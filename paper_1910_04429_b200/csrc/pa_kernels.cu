@@ -115,10 +115,17 @@ __global__ void k_pack(const uint8_t* __restrict__ in, long long in_stride, long
   u32* dst = words + (long long)b * word_stride;
   const long long nbytes = (n_bits + 7) >> 3;
   const long long kn = (n_bits + 31) >> 5;
+  // whole 4-byte words in place (LSF) or byte-reversed (MSF) when the row allows
+  const bool a4 = ((reinterpret_cast<uintptr_t>(src) & 3) == 0) && (msf ? (nbytes & 3) == 0 : true);
+  const long long kfull = nbytes >> 2;  // words made only of input bytes
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < kw;
        j += (long long)gridDim.x * blockDim.x) {
     u32 w = 0;
-    if (j < kn) {
+    if (a4 && j < kfull) {
+      const u32* s32 = reinterpret_cast<const u32*>(src);
+      w = msf ? __byte_perm(__ldg(s32 + (kfull - 1 - j)), 0u, 0x0123) : __ldg(s32 + j);
+      if (j == kn - 1 && (n_bits & 31)) w &= (1u << (n_bits & 31)) - 1u;
+    } else if (j < kn) {
       const long long q0 = 4 * j;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -140,6 +147,27 @@ __global__ void k_unpack(const u32* __restrict__ words, long long word_stride, l
   const u32* src = words + (long long)b * word_stride;
   uint8_t* dst = out + (long long)b * out_stride;
   const long long mb = (m_bits + 7) >> 3;
+  if (!msf && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {  // whole words where possible
+    const long long mw4 = mb >> 2;
+    u32* d32 = reinterpret_cast<u32*>(dst);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < mw4;
+         q += (long long)gridDim.x * blockDim.x)
+      d32[q] = src[q];
+    for (long long q = 4 * mw4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < mb;
+         q += (long long)gridDim.x * blockDim.x)
+      dst[q] = (uint8_t)(src[q >> 2] >> (8 * (q & 3)));
+    return;
+  }
+  if (!msf && (reinterpret_cast<uintptr_t>(dst) & 1) == 0) {  // 2-byte aligned rows: halves
+    const long long mh = mb >> 1;
+    uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < mh;
+         q += (long long)gridDim.x * blockDim.x)
+      d16[q] = (uint16_t)(src[q >> 1] >> (16 * (q & 1)));
+    if ((mb & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+      dst[mb - 1] = (uint8_t)(src[(mb - 1) >> 2] >> (8 * ((mb - 1) & 3)));
+    return;
+  }
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < mb;
        q += (long long)gridDim.x * blockDim.x) {
     const uint8_t byte = (uint8_t)(src[q >> 2] >> (8 * (q & 3)));
