@@ -29,6 +29,8 @@ struct OpView {
   int kc;
   u32 mlo, mhi;
   int cw;
+  bool a8;   // cw = 2: the row is 8-byte aligned (else two 4-byte loads per coefficient)
+  bool odd;  // cw = 2: odd word count, the last coefficient has no high word
 };
 __device__ __forceinline__ OpView op_view(const ConvJob& job, int op, int b) {
   OpView v;
@@ -36,6 +38,8 @@ __device__ __forceinline__ OpView op_view(const ConvJob& job, int op, int b) {
   const long long kv = op ? job.kX : job.kA;
   const u32 mask = op ? job.maskX : job.maskA;
   v.cw = job.cw;
+  v.a8 = (reinterpret_cast<uintptr_t>(v.src) & 7) == 0;
+  v.odd = (kv & 1) != 0;
   if (job.cw == 2) {
     v.kc = (int)((kv + 1) >> 1);
     v.mlo = (kv & 1) ? mask : 0xFFFFFFFFu;
@@ -54,11 +58,19 @@ __device__ __forceinline__ u32 coef_red(u32 lo, u32 hi, int cw) {
   if (cw == 1) return a;
   return red(a + shoup(hi, PK<P>::r32, PK<P>::r32_sh, PK<P>::p), PK<P>::two_p);
 }
+// the two words of 64-bit coefficient gi (cw = 2): one 8-byte load on 8-byte
+// aligned rows, else two 4-byte loads; the last coefficient of an odd word
+// count has no high word (it is not read: it may lie past the row)
+__device__ __forceinline__ uint2 ld_coef2(const OpView& o, int gi, bool last) {
+  if (last && o.odd) return make_uint2(__ldg(o.src + 2 * gi), 0u);
+  if (o.a8) return __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+  return make_uint2(__ldg(o.src + 2 * gi), __ldg(o.src + 2 * gi + 1));
+}
 // coefficient gi known to be valid and unmasked (gi < kc - 1)
 template <int P>
 __device__ __forceinline__ u32 coef_fast(const OpView& o, int gi) {
   if (o.cw == 2) {
-    const uint2 w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+    const uint2 w = ld_coef2(o, gi, false);
     return coef_red<P>(w.x, w.y, 2);
   }
   return coef_red<P>(__ldg(o.src + gi), 0u, 1);
@@ -69,7 +81,7 @@ __device__ __forceinline__ uint2 coef_raw_at(const OpView& o, int gi) {
   uint2 w = make_uint2(0u, 0u);
   if (gi < o.kc) {
     if (o.cw == 2) {
-      w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+      w = ld_coef2(o, gi, gi == o.kc - 1);
     } else {
       w.x = __ldg(o.src + gi);
     }
@@ -87,7 +99,7 @@ __device__ __forceinline__ u32 coef_at(const OpView& o, int gi) {
   u32 lo = 0u, hi = 0u;
   if (gi < o.kc) {
     if (o.cw == 2) {
-      const uint2 w = __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
+      const uint2 w = ld_coef2(o, gi, gi == o.kc - 1);
       lo = w.x;
       hi = w.y;
     } else {
@@ -147,7 +159,7 @@ __device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, in
                                               int lgC, int c0) {
   const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
-  if (ov.cw == 2 && ((rows - 1) << lgC) + c0 + CT - 1 < ov.kc - 1) {
+  if (ov.cw == 2 && ov.a8 && ((rows - 1) << lgC) + c0 + CT - 1 < ov.kc - 1) {
     // every staged coefficient valid and unmasked (all but the operand's last tiles)
     for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
       const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
@@ -161,7 +173,12 @@ __device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, in
     const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
     if (gi < ov.kc - 1) {
       if (ov.cw == 2) {
-        cp_async8(stage + e, ov.src + 2 * gi);
+        if (ov.a8) {
+          cp_async8(stage + e, ov.src + 2 * gi);
+        } else {
+          cp_async4(stage + e, ov.src + 2 * gi);
+          cp_async4(reinterpret_cast<u32*>(stage + e) + 1, ov.src + 2 * gi + 1);
+        }
       } else {
         cp_async4(stage + e, ov.src + gi);
         reinterpret_cast<u32*>(stage + e)[1] = 0u;
@@ -755,7 +772,8 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
                 if (row < srows) raw[s][k] = stage[(row << lct) + t];
               } else if (gi < ov.kc) {
                 if (ov.cw == 2) {
-                  raw[s][k] = __ldg(src2 + gi);
+                  raw[s][k] = ov.a8 && gi < ov.kc - 1 ? __ldg(src2 + gi)
+                                                      : ld_coef2(ov, gi, gi == ov.kc - 1);
                 } else {
                   raw[s][k].x = __ldg(ov.src + gi);
                 }

@@ -542,8 +542,9 @@ static int hash_batch_impl(const uint8_t* x, const uint8_t* c, const uint8_t* d,
     return fail(PAB_EINVAL, "split hashing needs the whole batch in one workspace");
   const int msf = byte_order == PAB_ORDER_MSF;
   // LSF blocks whose words can be read in place (the common case): no pack kernel
-  // (64-bit coefficients are read as 8-byte words: whole, 8-byte aligned rows)
-  const u64 al = 4 * (u64)g.md.cw;
+  // (64-bit coefficients are read as one 8-byte load where the row is 8-byte
+  // aligned, as two 4-byte loads elsewhere)
+  const u64 al = 4;
   const bool direct_in = !msf && nbytes % al == 0 && in_stride % al == 0 && aligned(x, al) &&
                          aligned(c, al) && aligned(d, al);
   const bool direct_out = !msf && out_stride % 4 == 0 && aligned(out, 4);

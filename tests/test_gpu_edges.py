@@ -115,3 +115,19 @@ def test_zero_batch_and_errors():
         _native.hash_host(b"\x01", b"\x01", b"\x01", 8, 9)
     with pytest.raises(ValueError):
         HashEngine(100, 0)
+
+
+@pytest.mark.parametrize("n", [500_000, 65_504, 4_000_032])
+def test_four_byte_aligned_rows_direct(n, coef_words):
+    # n = 32 mod 64: ceil(n/8) % 8 == 4, so rows alternate between 8- and 4-byte
+    # alignment and the word count is odd (the last 64-bit coefficient has no
+    # high word); read in place, without the pack kernel
+    rng = np.random.default_rng(n + 1)
+    B = 5
+    arr = _rand_blocks(rng, n, B)
+    dx, dc, dd = (torch.from_numpy(a).cuda() for a in arr)
+    for r in (n // 2, n - 7):
+        out = HashEngine(n, r, max_batch=B).hash_device(dx, dc, dd).cpu().numpy()
+        for i in range(B):
+            want = oracle.compress(*(arr[j, i].tobytes() for j in range(3)), n, r)
+            assert out[i].tobytes() == want, (n, r, i)
