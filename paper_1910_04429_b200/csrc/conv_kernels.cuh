@@ -757,60 +757,73 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
     // of each load was 25% of stall samples) and the known zeros fold away.
     if (ov.kc <= (L >> 1)) {
       const uint2* src2 = reinterpret_cast<const uint2*>(ov.src);
-      for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
-        const int t = task & (CT - 1), o = task >> lct;
-        uint2 raw[M][NK];
+      auto pass = [&](auto s8_c) {
+        constexpr bool S8 = decltype(s8_c)::value;
+        for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {
+          const int t = task & (CT - 1), o = task >> lct;
+          // every loaded coefficient of the task below kc - 1: no checks, no mask
+          const int gtop = ((o + ((NK / 2 - 1) << SLO0) + (M / 2) * R2) << lgC) + c0 + t;
+          const bool inner = !STAGED && S8 && gtop < ov.kc - 1;
+          uint2 raw[M][NK];
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {
+          for (int k = 0; k < NK; ++k) {
 #pragma unroll
-          for (int s = 0; s < M; ++s) {
-            raw[s][k] = make_uint2(0u, 0u);
-            if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
-              const int row = o + (k << SLO0) + s * R2;
-              const int gi = (row << lgC) + c0 + t;
-              if (STAGED) {  // staged raw words (last one already masked)
-                if (row < srows) raw[s][k] = stage[(row << lct) + t];
-              } else if (gi < ov.kc) {
-                if (ov.cw == 2) {
-                  raw[s][k] = ov.a8 && gi < ov.kc - 1 ? __ldg(src2 + gi)
-                                                      : ld_coef2(ov, gi, gi == ov.kc - 1);
-                } else {
-                  raw[s][k].x = __ldg(ov.src + gi);
+            for (int s = 0; s < M; ++s) {
+              raw[s][k] = make_uint2(0u, 0u);
+              if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
+                const int row = o + (k << SLO0) + s * R2;
+                const int gi = (row << lgC) + c0 + t;
+                if (STAGED) {  // staged raw words (last one already masked)
+                  if (row < srows) raw[s][k] = stage[(row << lct) + t];
+                } else if (inner) {
+                  raw[s][k] = __ldg(src2 + gi);
+                } else if (gi < ov.kc) {
+                  if (ov.cw == 2) {
+                    // S8: 8-byte rows of whole coefficients (one 8-byte load each)
+                    raw[s][k] = S8 ? __ldg(src2 + gi) : ld_coef2(ov, gi, gi == ov.kc - 1);
+                  } else {
+                    raw[s][k].x = __ldg(ov.src + gi);
+                  }
                 }
               }
             }
           }
-        }
-        u32 v[M][NK];
+          u32 v[M][NK];
 #pragma unroll
-        for (int k = 0; k < NK; ++k) {
-          const int j = o + (k << SLO0);
-          u32 a[M];
+          for (int k = 0; k < NK; ++k) {
+            const int j = o + (k << SLO0);
+            u32 a[M];
 #pragma unroll
-          for (int s = 0; s < M; ++s) {
-            if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
-              const int gi = ((j + s * R2) << lgC) + c0 + t;
-              uint2 w = raw[s][k];
-              if (!STAGED && gi == ov.kc - 1) {
-                w.x &= ov.mlo;
-                w.y &= ov.mhi;
+            for (int s = 0; s < M; ++s) {
+              if (s < M / 2 || (s == M / 2 && k < NK / 2)) {
+                const int gi = ((j + s * R2) << lgC) + c0 + t;
+                uint2 w = raw[s][k];
+                if (!STAGED && !inner && gi == ov.kc - 1) {
+                  w.x &= ov.mlo;
+                  w.y &= ov.mhi;
+                }
+                a[s] = coef_red<P>(w.x, w.y, ov.cw);
+              } else {
+                a[s] = 0u;
               }
-              a[s] = coef_red<P>(w.x, w.y, ov.cw);
-            } else {
-              a[s] = 0u;
             }
+            radix_m<P, M, false>(a);
+#pragma unroll
+            for (int s = 0; s < M; ++s)
+              v[s][k] = s ? shoup(a[s], __ldg(trad + j * s), PK<P>::p) : a[0];
           }
-          radix_m<P, M, false>(a);
+          dif_rt<P, RS0, SLO0, M>(v, twf + o);
 #pragma unroll
           for (int s = 0; s < M; ++s)
-            v[s][k] = s ? shoup(a[s], __ldg(trad + j * s), PK<P>::p) : a[0];
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+              smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t] = v[s][k];
         }
-        dif_rt<P, RS0, SLO0, M>(v, twf + o);
-#pragma unroll
-        for (int s = 0; s < M; ++s)
-#pragma unroll
-          for (int k = 0; k < NK; ++k)
-            smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t] = v[s][k];
+      };
+      if (ov.a8 && !ov.odd) {
+        pass(std::integral_constant<bool, true>{});
+      } else {
+        pass(std::integral_constant<bool, false>{});
       }
     } else
     for (int task = threadIdx.x; task < (CT << SLO0); task += blockDim.x) {

@@ -827,6 +827,9 @@ __global__ void __launch_bounds__(kWThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob
       DV[2 * w] = v.x;
       DV[2 * w + 1] = v.y;
     }
+  } else if (lw + kWLw < kd) {  // 4-byte aligned rows, whole words (the last one is masked)
+#pragma unroll
+    for (int w = 0; w < kWLw; ++w) DV[w] = __ldg(dw + lw + w);
   } else {
 #pragma unroll
     for (int w = 0; w < kWLw; ++w) DV[w] = fetch_word(dw, lw + w, kd, job.maskD);
