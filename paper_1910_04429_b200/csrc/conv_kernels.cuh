@@ -856,7 +856,40 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
       __syncthreads();
     }
   } else {
-  // radix-M stage straight from the operand words
+  // radix-M stage straight from the operand words.  kc <= L/2 (the hash): rows
+  // >= R/2 are zero -- sub-columns s > M/2 always, s = M/2 for j >= R2/2 -- so
+  // the two halves of j run as compile-time variants with only the nonzero
+  // loads, all issued first (plain 8-byte loads where the task is inside kc - 1)
+  auto radix_task = [&](auto hi_c, int task) {
+    constexpr bool HI = decltype(hi_c)::value;  // j >= R2/2
+    const int t = task & (CT - 1), j = task >> lct;
+    constexpr int STOP = HI ? M / 2 : M / 2 + 1;  // sub-columns s < STOP can be nonzero
+    const int gtop = ((j + (STOP - 1) * R2) << lgC) + c0 + t;
+    const bool fast = ov.cw == 2 && ov.a8 && gtop < ov.kc - 1;
+    uint2 raw[M];
+#pragma unroll
+    for (int s = 0; s < M; ++s) {
+      raw[s] = make_uint2(0u, 0u);
+      if (s < STOP) {
+        const int gi = ((j + s * R2) << lgC) + c0 + t;
+        raw[s] = fast ? __ldg(reinterpret_cast<const uint2*>(ov.src) + gi) : coef_raw_at(ov, gi);
+      }
+    }
+    u32 a[M];
+#pragma unroll
+    for (int s = 0; s < M; ++s) a[s] = s < STOP ? coef_red<P>(raw[s].x, raw[s].y, ov.cw) : 0u;
+    radix_m<P, M, false>(a);
+#pragma unroll
+    for (int s = 1; s < M; ++s) a[s] = shoup(a[s], __ldg(trad + j * s), PK<P>::p);
+#pragma unroll
+    for (int s = 0; s < M; ++s) smem[(s * T2 + sm_idx(j)) * CT + t] = a[s];
+  };
+  if (!STAGED && ov.kc <= (L >> 1)) {
+    for (int task = threadIdx.x; task < (CT << (LGR2 - 1)); task += blockDim.x)
+      radix_task(std::integral_constant<bool, false>{}, task);
+    for (int task = (CT << (LGR2 - 1)) + threadIdx.x; task < (CT << LGR2); task += blockDim.x)
+      radix_task(std::integral_constant<bool, true>{}, task);
+  } else {
   for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
     const int t = task & (CT - 1), j = task >> lct;
     u32 a[M];
@@ -870,6 +903,7 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
     for (int s = 1; s < M; ++s) a[s] = shoup(a[s], __ldg(trad + j * s), PK<P>::p);
 #pragma unroll
     for (int s = 0; s < M; ++s) smem[(s * T2 + sm_idx(j)) * CT + t] = a[s];
+  }
   }
   __syncthreads();
   if constexpr (PP.n >= 2) {
