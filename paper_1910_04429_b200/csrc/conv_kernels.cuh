@@ -1016,8 +1016,13 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
     colm_pass<P, M, LGR2, PP.rs[0], PP.slo[0], false>(smem, lct, twi);
     __syncthreads();
   }
-  // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT -> canonical residues
-  for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x) {
+  // inverse radix-M stage: twiddle w_R^(-j*s), inverse DFT -> canonical residues.
+  // nres <= L/2 (the hash): rows >= R/2 are never stored -- sub-columns s > M/2,
+  // and s = M/2 for j >= R2/2 -- so the two halves of j run as compile-time
+  // variants and the dead outputs fold away
+  auto inv_task = [&](auto mode_c, int task) {
+    constexpr int MODE = decltype(mode_c)::value;  // 0: all outputs, 1: j < R2/2, 2: j >= R2/2
+    constexpr int STOP = MODE == 0 ? M : (MODE == 1 ? M / 2 + 1 : M / 2);
     const int t = task & (CT - 1), j = task >> lct;
     u32 a[M];
     a[0] = red(smem[sm_idx(j) * CT + t], PK<P>::two_p);
@@ -1026,10 +1031,19 @@ __device__ __forceinline__ void colm_inv_body(const ConvJob& job, const PlanTabl
       a[s] = shoup(smem[(s * T2 + sm_idx(j)) * CT + t], __ldg(trad + j * s), PK<P>::p);
     radix_m<P, M, true>(a);
 #pragma unroll
-    for (int s = 0; s < M; ++s) {
+    for (int s = 0; s < STOP; ++s) {
       const int gi = ((j + s * R2) << lgC) + c0 + t;
       if (gi < nres) res[gi] = red(a[s], PK<P>::p);  // [0, 2p) -> canonical; scale in the twiddles
     }
+  };
+  if (job.nRes <= (L >> 1)) {
+    for (int task = threadIdx.x; task < (CT << (LGR2 - 1)); task += blockDim.x)
+      inv_task(std::integral_constant<int, 1>{}, task);
+    for (int task = (CT << (LGR2 - 1)) + threadIdx.x; task < (CT << LGR2); task += blockDim.x)
+      inv_task(std::integral_constant<int, 2>{}, task);
+  } else {
+    for (int task = threadIdx.x; task < (CT << LGR2); task += blockDim.x)
+      inv_task(std::integral_constant<int, 0>{}, task);
   }
 }
 
