@@ -548,7 +548,23 @@ __device__ __forceinline__ void col_fwd_body(const ConvJob& job, const PlanTable
       } else if (half) {
         const int g0 = (o << lgC) + col;
         constexpr int kTop = ((1 << (RS0 - 1)) - 1) << (SLO0 + lgC);
-        if (g0 + kTop < ilast) {  // every coefficient of the task is valid and unmasked
+        if (g0 + kTop < ilast && ov.cw == 2) {  // every coefficient valid and unmasked:
+          // all loads first (8-byte rows: one load each), then the reductions
+          uint2 raw[1 << (RS0 - 1)];
+          if (ov.a8) {
+            const uint2* s2 = reinterpret_cast<const uint2*>(ov.src);
+#pragma unroll
+            for (int k = 0; k < (1 << (RS0 - 1)); ++k) raw[k] = __ldg(s2 + g0 + (k << (SLO0 + lgC)));
+          } else {
+#pragma unroll
+            for (int k = 0; k < (1 << (RS0 - 1)); ++k) {
+              const u32* w = ov.src + 2 * (g0 + (k << (SLO0 + lgC)));
+              raw[k] = make_uint2(__ldg(w), __ldg(w + 1));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < (1 << (RS0 - 1)); ++k) v[0][k] = coef_red<P>(raw[k].x, raw[k].y, 2);
+        } else if (g0 + kTop < ilast) {
 #pragma unroll
           for (int k = 0; k < (1 << (RS0 - 1)); ++k)
             v[0][k] = coef_fast<P>(ov, g0 + (k << (SLO0 + lgC)));
