@@ -62,9 +62,12 @@ __device__ __forceinline__ u32 coef_red(u32 lo, u32 hi, int cw) {
 // aligned rows, else two 4-byte loads; the last coefficient of an odd word
 // count has no high word (it is not read: it may lie past the row)
 __device__ __forceinline__ uint2 ld_coef2(const OpView& o, int gi, bool last) {
-  if (last && o.odd) return make_uint2(__ldg(o.src + 2 * gi), 0u);
-  if (o.a8) return __ldg(reinterpret_cast<const uint2*>(o.src) + gi);
-  return make_uint2(__ldg(o.src + 2 * gi), __ldg(o.src + 2 * gi + 1));
+  // two 4-byte loads, the second predicated (no branch between loads, so the
+  // compiler can issue a task's loads together); hot paths use 8-byte loads directly
+  const u32* w = o.src + 2 * gi;
+  const u32 lo = __ldg(w);
+  const u32 hi = (last && o.odd) ? 0u : __ldg(w + 1);
+  return make_uint2(lo, hi);
 }
 // coefficient gi known to be valid and unmasked (gi < kc - 1)
 template <int P>
