@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kWThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob
 
   // residues -> CRT of coefficients cb .. cb + 7
   u32 X[kWCpt][5];
-  if (cb >= 0 && cb + kWCpt <= nres && (cb & 3) == 0 && (L & 3) == 0) {
+  if (kWCpt % 4 == 0 && cb >= 0 && cb + kWCpt <= nres && (cb & 3) == 0 && (L & 3) == 0) {
     // 16-byte quads (cb mod 4 is warp-uniform: half the warps)
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
