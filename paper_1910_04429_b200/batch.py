@@ -238,6 +238,8 @@ class HashEngine:
 
     def _slot_events(self, k: int):
         if getattr(self, "_ev_k", None) != k:
+            if getattr(self, "_ev_k", None) is not None:
+                self.join()  # earlier calls' copies / hashing may still wait on the old events
             mk = lambda: [torch.cuda.Event() for _ in range(k)]  # noqa: E731
             self._ev = {"in": mk(), "comp": mk(), "out": mk(), "seed": mk()}
             self._ev_k = k
@@ -246,6 +248,10 @@ class HashEngine:
     def _io_buffers(self, k: int, chunk: int):
         key = (k, chunk)
         if getattr(self, "_io_key", None) != key:
+            if getattr(self, "_io_key", None) is not None:
+                # a join_out=False call may still be copying into / hashing from the
+                # old slots: the allocator must not hand their memory out before that
+                torch.cuda.synchronize(self.device)
             mk = lambda w: torch.empty((chunk, w), dtype=torch.uint8, device=self.device)  # noqa: E731
             self._io = [(mk(self.nbytes), mk(self.nbytes), mk(self.nbytes), mk(self.rbytes))
                         for _ in range(k)]

@@ -123,6 +123,29 @@ def run_bench(cfg: RunConfig, *, quiet: bool = False, scope: str | None = None) 
     ]
 
 
+def measure_ratio_spread(n: int, ratios: tuple[float, ...] = (0.125, 0.5, 0.9),
+                         trials: int = 11, rng_seed: int = 0) -> dict[float, float]:
+    """Best drop-in round time per compression ratio at one block size (bench.py:185-208).
+
+    Trials interleave over the ratios; the first interleaved pass is warm-up
+    and the minimum per ratio is reported (scheduling noise only adds).
+    """
+    cfg = RunConfig(sizes=(n,), rng_seed=rng_seed)
+    raw = pa.export_block(bench_input(cfg, n), cfg.order)
+    seed = pa.gen_seed(n, pa.derive_block_seed(rng_seed, n))
+    best: dict[float, float] = {}
+    for trial in range(trials + 1):
+        for ratio in ratios:
+            params = pa.PAParams(n=n, r=max(1, int(ratio * n)))
+            t0 = time.perf_counter()
+            out = pa.pa_round(pa.import_block(raw, n, cfg.order), params, seed, enforce=False)
+            pa.export_block(out, cfg.order)
+            dt = time.perf_counter() - t0
+            if trial:
+                best[ratio] = min(best.get(ratio, dt), dt)
+    return best
+
+
 def _bench_row(rec: BenchRecord) -> dict:
     return {"block_size": rec.block_size, "algorithm": rec.algorithm, "trials": rec.trials,
             "elapsed_ms": round(rec.elapsed_median * 1e3, 6),

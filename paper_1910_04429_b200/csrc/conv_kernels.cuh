@@ -839,7 +839,7 @@ __device__ __forceinline__ void colm_fwd_body(const ConvJob& job, const PlanTabl
               smem[(s * T2 + sm_idx(o + (k << SLO0))) * CT + t] = v[s][k];
         }
       };
-      if (ov.a8 && !ov.odd) {
+      if (ov.cw == 2 && ov.a8 && !ov.odd) {  // S8 = whole 8-byte coefficients only
         pass(std::integral_constant<bool, true>{});
       } else {
         pass(std::integral_constant<bool, false>{});

@@ -51,6 +51,12 @@ class RunConfig:
     order: WordOrder = WordOrder.LEAST_SIGNIFICANT_FIRST
     trials: int = 5
     timing: str = "pipeline"
+    # accepted for drop-in compatibility (bench.py:72-76); plots and the
+    # universality audit are outside the hash path and ignore-only here
+    plot: bool = True
+    alpha: int = 6
+    beta: int = 3
+    seed_sample: int | None = None
 
     def __post_init__(self) -> None:
         if self.out_bits is not None and self.ratio is not None:
@@ -87,7 +93,7 @@ class PaRunResult:
     blocks: int
     n: int
     r: int
-    budget: object | None
+    budget: security.SecurityBudget | None
     out_path: str
 
 
@@ -95,17 +101,30 @@ class PaRunResult:
 Hasher = Callable[[np.ndarray, np.ndarray, np.ndarray, int, int, WordOrder], np.ndarray]
 
 
+def _default_devices() -> list[int]:
+    """Every visible GPU; under torch.distributed a rank owns only its current one."""
+    import torch
+    import torch.distributed as tdist
+
+    if tdist.is_available() and tdist.is_initialized():
+        return [torch.cuda.current_device()]
+    n = torch.cuda.device_count()
+    if n == 0:
+        raise _native.NativeUnavailable("no CUDA device visible (there is no CPU fallback)")
+    return list(range(n))
+
+
 def gpu_hasher(batch: int = 256, devices: list[int] | None = None) -> Hasher:
     """Default hasher: the CUDA path over pinned staging.  `devices` = GPUs of this
-    process to shard each batch over (default: the current device only; under
-    torch.distributed every rank owns one GPU)."""
+    process to shard each batch over (default: every visible GPU, block-sharded
+    with no inter-GPU traffic; under torch.distributed every rank owns one GPU)."""
 
     def run(x, c, d, n, r, order):
         import torch
 
         from .batch import hash_host_multi
 
-        devs = devices if devices is not None else [torch.cuda.current_device()]
+        devs = devices if devices is not None else _default_devices()
         px, pc, pd = (torch.from_numpy(np.array(a, copy=True)).pin_memory() for a in (x, c, d))
         out = hash_host_multi(px, pc, pd, n, r, devices=devs, max_batch=batch,
                               order=_native.ORDER_MSF if order is WordOrder.MOST_SIGNIFICANT_FIRST
@@ -130,7 +149,7 @@ def gpu_seeded_hasher(batch: int = 256, devices: list[int] | None = None) -> See
 
         from .batch import hash_host_multi
 
-        devs = devices if devices is not None else [torch.cuda.current_device()]
+        devs = devices if devices is not None else _default_devices()
         px = torch.from_numpy(np.array(x, copy=True)).pin_memory()
         out = hash_host_multi(px, None, None, n, r, devices=devs, max_batch=batch,
                               rng_seed=rng_seed, first_index=first_index,
@@ -204,11 +223,13 @@ def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
         check = security.validate(params)
         if not check.ok:
             raise pa.SecurityBoundError(params.r, check.r_max)
-        budget = {"h_min": cfg.h_min, "epsilon": cfg.epsilon, "r": r,
-                  "eps_bar_log2": security.leftover_bound_log2(cfg.h_min, r, cfg.epsilon)}
+        budget = security.SecurityBudget.evaluate(cfg.h_min, cfg.epsilon, r)
 
     if hasher is None and seeded is None:
-        seeded = gpu_seeded_hasher()
+        if len(_native.seed_material(cfg.rng_seed)) <= _native.MAX_SEED_MATERIAL:
+            seeded = gpu_seeded_hasher()
+        else:  # the device expander absorbs <= 1 KiB of master material: expand on the host
+            hasher = gpu_hasher()
     lo, hi = shard_range(nblocks, rank, world)
     arr = np.frombuffer(data, np.uint8, count=nblocks * block_bytes).reshape(nblocks, block_bytes)
     rb = (r + 7) // 8

@@ -261,3 +261,24 @@ print("SEQ_OK")
     res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert res.returncode == 0 and "SEQ_OK" in res.stdout, res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n,cw", [(200_000_000, 0), (45_505_408, 1)])
+def test_fused_mixed_radix_forward_with_32bit_coefficients(n, cw):
+    # the fused radix-3 forward pass at (m=3, lgR=10, lgC=12)
+    # must not take its 8-byte-coefficient fast path for 32-bit coefficients with
+    # an even word count (n = 2e8 by default plan; 45,505,408 with cw forced to 1)
+    assert (n // 32) % 2 == 0
+    _native.force_coef_words(cw)
+    try:
+        rng = random.Random(n)
+        nb = n // 8
+        x = rng.randbytes(nb)
+        c = bytearray(rng.randbytes(nb))
+        c[0] |= 1
+        d = rng.randbytes(nb)
+        for r in (n // 2, 1_000_003):
+            got = _native.hash_host(x, bytes(c), d, n, r)
+            assert got == oracle.compress(x, bytes(c), d, n, r), (n, cw, r, _native.plan_info(n))
+    finally:
+        _native.force_coef_words(0)
