@@ -103,6 +103,32 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
                   uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device);
 
 /*
+ * Host hash over CPython integer digits (the drop-in compress / pa_round path
+ * with Python ints, pkg/src/modpa/pa.py:175-217): x, c, d are magnitudes as
+ * 30-bit digits in 32-bit slots, least significant first (CPython's own int
+ * layout, sys.int_info.bits_per_digit == 30), x_nd / c_nd / d_nd digits each
+ * (missing high digits are zero, bits >= n ignored).  out receives out_nd >=
+ * ceil(r/30) digits of the key (not normalized: high digits may be zero).
+ * The digit <-> word conversion runs on the GPU.  Blocks until done.
+ */
+int pab_hash_digits(const uint32_t* x, uint64_t x_nd, const uint32_t* c, uint64_t c_nd,
+                    const uint32_t* d, uint64_t d_nd, uint64_t n_bits, uint64_t r_bits,
+                    uint32_t* out, uint64_t out_nd, int device);
+
+/*
+ * Host layout conversions of the drop-in boundary (import_block /
+ * export_block, pkg/src/modpa/pa.py:111-132): CPython int digits (30-bit
+ * payload in 32-bit slots, least significant first) <-> nbytes serialized
+ * bytes in byte_order.  pab_digits_to_bytes writes exactly nbytes bytes (bits
+ * beyond them are dropped, missing digits are zero); pab_bytes_to_digits fills
+ * nd digits (zero beyond the input).  Pure host code, no device involved.
+ */
+int pab_digits_to_bytes(const uint32_t* dig, uint64_t nd, uint8_t* out, uint64_t nbytes,
+                        int byte_order);
+int pab_bytes_to_digits(const uint8_t* in, uint64_t nbytes, int byte_order, uint32_t* dig,
+                        uint64_t nd);
+
+/*
  * One batch hashed with its NTT primes split over several GPUs (SURVEY.md
  * §8f: single-block multi-GPU).  The convolution modulo each prime is
  * independent, so share s of `ndev` computes the residues for its contiguous
@@ -150,6 +176,21 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
             void* workspace, size_t workspace_bytes, void* stream);
 int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes,
                  uint8_t* out, int device);
+
+/*
+ * Fused multiply-add (bignum.fused_mul_add, pkg/src/modpa/bignum.py:234-238):
+ * out = acc + a*b over LSF byte strings, out_bytes >= max(a_bytes + b_bytes,
+ * acc_bytes) + 1 (zero padded).  The addend rides in the carry kernel (the
+ * hash's +d); no truncation.  Device variant asynchronous on `stream`; the
+ * host variant blocks, like pab_mul_host.
+ */
+size_t pab_mul_add_workspace_bytes(uint64_t acc_bytes, uint64_t a_bytes, uint64_t b_bytes);
+int pab_mul_add(const uint8_t* acc, uint64_t acc_bytes, const uint8_t* a, uint64_t a_bytes,
+                const uint8_t* b, uint64_t b_bytes, uint8_t* out, uint64_t out_bytes,
+                void* workspace, size_t workspace_bytes, void* stream);
+int pab_mul_add_host(const uint8_t* acc, uint64_t acc_bytes, const uint8_t* a, uint64_t a_bytes,
+                     const uint8_t* b, uint64_t b_bytes, uint8_t* out, uint64_t out_bytes,
+                     int device);
 
 /*
  * Optional per-kernel timing: while enabled, CUDA events are recorded on the

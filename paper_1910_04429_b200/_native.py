@@ -40,6 +40,13 @@ SIGNATURES = {
                                       ctypes.c_uint64, _u8p, ctypes.c_size_t, _u8p]),
     "pab_hash_host": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_int]),
+    "pab_hash_digits": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
+                                       ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u8p,
+                                       ctypes.c_uint64, ctypes.c_int]),
+    "pab_digits_to_bytes": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64,
+                                           ctypes.c_int]),
+    "pab_bytes_to_digits": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_int, _u8p,
+                                           ctypes.c_uint64]),
     "pab_hash_host_split": (ctypes.c_int, [_u8p, _u8p, _u8p, ctypes.c_uint64, ctypes.c_uint64,
                                            ctypes.c_uint32, ctypes.c_int, _u8p,
                                            ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
@@ -54,6 +61,12 @@ SIGNATURES = {
                                ctypes.c_size_t, _u8p]),
     "pab_mul_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
                                     ctypes.c_int]),
+    "pab_mul_add_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64] * 3),
+    "pab_mul_add": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
+                                   ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p, ctypes.c_size_t,
+                                   _u8p]),
+    "pab_mul_add_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p,
+                                        ctypes.c_uint64, _u8p, ctypes.c_uint64, ctypes.c_int]),
     "pab_profile_enable": (None, [ctypes.c_int]),
     "pab_profile_collect": (ctypes.c_int, [ctypes.POINTER(ctypes.c_char_p),
                                            ctypes.POINTER(ctypes.c_int),
@@ -115,6 +128,22 @@ def hash_host(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
     return out.raw
 
 
+def hash_ints(x: int, c: int, d: int, n: int, r: int, device: int | None = None) -> int:
+    """The key of one block given as Python ints: digits in, digits out (pab_hash_digits);
+    no int <-> bytes conversion on the host."""
+    from . import _pyint
+
+    lib = load()
+    dev = _device() if device is None else device
+    xa, xn = _pyint.digits(x)
+    ca, cn = _pyint.digits(c)
+    da, dn = _pyint.digits(d)
+    ond = (r + 29) // 30
+    out, oa = _pyint.new_uninit(ond)
+    check(lib.pab_hash_digits(xa, xn, ca, cn, da, dn, n, r, oa, ond, dev))
+    return _pyint.normalize(out, ond)
+
+
 def hash_host_split(x: bytes, c: bytes, d: bytes, n: int, r: int, batch: int = 1,
                     order: int = ORDER_LSF, devices: list[int] | None = None) -> bytes:
     """As hash_host, with the NTT primes of the convolution split over `devices`
@@ -156,6 +185,16 @@ def mul_host(a: bytes, b: bytes, device: int | None = None) -> bytes:
     dev = _device() if device is None else device
     out = ctypes.create_string_buffer(len(a) + len(b))
     check(lib.pab_mul_host(a, len(a), b, len(b), out, dev))
+    return out.raw
+
+
+def mul_add_host(acc: bytes, a: bytes, b: bytes, device: int | None = None) -> bytes:
+    """acc + a*b over LSF byte strings, max(len(a) + len(b), len(acc)) + 1 bytes."""
+    lib = load()
+    dev = _device() if device is None else device
+    ob = max(len(a) + len(b), len(acc)) + 1
+    out = ctypes.create_string_buffer(ob)
+    check(lib.pab_mul_add_host(acc, len(acc), a, len(a), b, len(b), out, ob, dev))
     return out.raw
 
 

@@ -182,5 +182,14 @@ def mul(a: BigNatLike, b: BigNatLike,
 def fused_mul_add(acc: BigNatLike, c: BigNatLike, x: BigNatLike,
                   alg: MulAlgorithm = MulAlgorithm.AUTO,
                   thresholds: ThresholdTable = DEFAULT_THRESHOLDS) -> BigNat:
-    """acc + c*x (bignum.py:234-238)."""
-    return BigNat(_as_int(acc) + mul(c, x, alg, thresholds).value)
+    """acc + c*x on the GPU (bignum.py:234-238): one call, the addend carried in
+    the product's carry kernel (the hash's +d) instead of a host add."""
+    av, cv, xv = _as_int(acc), _as_int(c), _as_int(x)
+    if not isinstance(alg, MulAlgorithm):
+        raise ValueError(f"unknown algorithm {alg!r}")
+    if cv == 0 or xv == 0:
+        return BigNat(av)
+    nb = lambda v: (v.bit_length() + 7) // 8  # noqa: E731
+    raw = _native.mul_add_host(av.to_bytes(nb(av), "little"), cv.to_bytes(nb(cv), "little"),
+                               xv.to_bytes(nb(xv), "little"))
+    return BigNat(int.from_bytes(raw, "little"))

@@ -164,6 +164,8 @@ struct HostCtx {  // cached buffers for the host-pointer entry points
   size_t ws_bytes = 0;
   uint8_t* dev_io = nullptr;
   size_t dev_io_bytes = 0;
+  uint8_t* pinned = nullptr;      // pinned staging of the Python-int digit path
+  size_t pinned_bytes = 0;
   std::mutex mu;
 };
 
@@ -609,7 +611,7 @@ static int hash_batch_impl(const uint8_t* x, const uint8_t* c, const uint8_t* d,
 // ================================================================== C ABI
 extern "C" {
 
-int pab_version(void) { return 101; }
+int pab_version(void) { return 102; }
 
 const char* pab_last_error(void) { return g_err.c_str(); }
 
@@ -735,6 +737,69 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
                        h.stream),
      "D2H out");
   CK(cudaStreamSynchronize(h.stream), "synchronize");
+  return PAB_OK;
+}
+
+int pab_hash_digits(const uint32_t* x, uint64_t x_nd, const uint32_t* c, uint64_t c_nd,
+                    const uint32_t* d, uint64_t d_nd, uint64_t n_bits, uint64_t r_bits,
+                    uint32_t* out, uint64_t out_nd, int device) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, r_bits, &g);
+  if (rc) return rc;
+  if ((x_nd && !x) || (c_nd && !c) || (d_nd && !d) || (out_nd && !out))
+    return fail(PAB_EINVAL, "null digit array");
+  const u64 ndn = ceil_div(n_bits, 30);
+  if (out_nd < ceil_div(r_bits, 30)) return fail(PAB_EINVAL, "out_nd must be >= ceil(r/30)");
+  // digits >= ceil(n/30) only carry bits >= n, which the hash ignores
+  const u64 xn = x_nd < ndn ? x_nd : ndn, cn = c_nd < ndn ? c_nd : ndn,
+            dn = d_nd < ndn ? d_nd : ndn;
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  DevState* ds;
+  if ((rc = ensure_device(device, &ds))) return rc;
+  HostCtx& h = ds->host;
+  std::lock_guard<std::mutex> lk(h.mu);
+  const u64 K = ceil_div(n_bits, 32);
+  const u64 in_stride = round_up(4 * K, 16);  // bytes per operand row (words)
+  const u64 rbytes = ceil_div(r_bits, 8), out_stride = round_up(rbytes, 16);
+  const u64 dig_in = 4 * (xn + cn + dn), dig_out = 4 * out_nd;
+  const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, 1);
+  const size_t io_bytes = 3 * in_stride + round_up(dig_in, 256) + out_stride + round_up(dig_out, 256);
+  if ((rc = host_ensure(h, ws_bytes, io_bytes))) return rc;
+  const size_t pin_bytes = round_up(dig_in, 256) + round_up(dig_out, 256);
+  if (h.pinned_bytes < pin_bytes) {
+    if (h.pinned) cudaFreeHost(h.pinned);
+    h.pinned = nullptr;
+    h.pinned_bytes = 0;
+    CK(cudaHostAlloc((void**)&h.pinned, pin_bytes, cudaHostAllocDefault), "pinned alloc");
+    h.pinned_bytes = pin_bytes;
+  }
+  uint8_t* words = h.dev_io;                        // x, c, d rows
+  uint8_t* ddig = words + 3 * in_stride;            // input digits
+  uint8_t* dout = ddig + round_up(dig_in, 256);     // key bytes (LSF, 16-byte padded)
+  uint8_t* dodig = dout + out_stride;               // key digits
+  uint8_t* pin_out = h.pinned + round_up(dig_in, 256);
+  std::memcpy(h.pinned, x, 4 * xn);
+  std::memcpy(h.pinned + 4 * xn, c, 4 * cn);
+  std::memcpy(h.pinned + 4 * (xn + cn), d, 4 * dn);
+  if (dig_in) CK(cudaMemcpyAsync(ddig, h.pinned, dig_in, cudaMemcpyHostToDevice, h.stream), "H2D");
+  DigitOperands ops;
+  ops.d[0] = (const u32*)ddig;
+  ops.d[1] = ops.d[0] + xn;
+  ops.d[2] = ops.d[1] + cn;
+  ops.nd[0] = (long long)xn;
+  ops.nd[1] = (long long)cn;
+  ops.nd[2] = (long long)dn;
+  launch_digits_pack(ops, 3, (long long)n_bits, (u32*)words, (long long)(in_stride / 4),
+                     (long long)K, h.stream);
+  rc = pab_hash_batch(words, words + in_stride, words + 2 * in_stride, in_stride, n_bits, r_bits,
+                      1, PAB_ORDER_LSF, dout, out_stride, h.ws, h.ws_bytes, h.stream);
+  if (rc) return rc;
+  launch_digits_unpack((const u32*)dout, (long long)r_bits, (u32*)dodig, (long long)out_nd,
+                       h.stream);
+  CK(cudaGetLastError(), "kernel launch");
+  CK(cudaMemcpyAsync(pin_out, dodig, dig_out, cudaMemcpyDeviceToHost, h.stream), "D2H");
+  CK(cudaStreamSynchronize(h.stream), "synchronize");
+  std::memcpy(out, pin_out, dig_out);
   return PAB_OK;
 }
 
@@ -923,30 +988,47 @@ int pab_hash_host_split(const uint8_t* x, const uint8_t* c, const uint8_t* d, ui
   return PAB_OK;
 }
 
-size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes) {
-  const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4);
-  if (ka == 0 || kb == 0) return 256;
-  const u64 nT = ka + kb;
-  Mode md;
-  if (!choose_mode(ka, kb, &md)) return 0;
-  return layout_for(ka > kb ? ka : kb, md.geo.L, nT, nT, 1, md.np).total;
+// out = acc + a*b over LSF byte strings (acc may be absent).  The product's
+// convolution is the hash's; the addend enters the carry kernel as its D
+// operand (the hash's +d), and nothing is truncated (n_mod_bits = 32 nT).
+static u64 mul_add_words(u64 ka, u64 kb, u64 kacc, u64 out_bytes) {
+  const u64 need = (ka + kb > kacc ? ka + kb : kacc) + (kacc ? 1 : 0);
+  const u64 have = ceil_div(out_bytes, 4);
+  return have > need ? have : need;
 }
 
-int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes, uint8_t* out,
-            void* workspace, size_t workspace_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+static size_t mul_add_ws(u64 acc_bytes, u64 a_bytes, u64 b_bytes, u64 out_bytes) {
+  const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4), kc = ceil_div(acc_bytes, 4);
+  if (ka == 0 || kb == 0) return 256;
+  Mode md;
+  if (!choose_mode(ka, kb, &md)) return 0;
+  const u64 nT = mul_add_words(ka, kb, kc, out_bytes);
+  u64 kmax = ka > kb ? ka : kb;
+  kmax = kmax > kc ? kmax : kc;
+  return layout_for(kmax, md.geo.L, nT, nT, 1, md.np).total;
+}
+
+static int mul_add_core(const uint8_t* acc, u64 acc_bytes, const uint8_t* a, u64 a_bytes,
+                        const uint8_t* b, u64 b_bytes, uint8_t* out, u64 out_bytes,
+                        void* workspace, size_t workspace_bytes, cudaStream_t st) {
   const u64 ka = ceil_div(a_bytes, 4), kb = ceil_div(b_bytes, 4);
-  if (a_bytes + b_bytes == 0) return PAB_OK;
-  if (ka == 0 || kb == 0) {
-    CK(cudaMemsetAsync(out, 0, a_bytes + b_bytes, st), "memset");
+  const u64 kc = acc ? ceil_div(acc_bytes, 4) : 0;
+  if (out_bytes == 0) return PAB_OK;
+  if (ka == 0 || kb == 0) {  // zero product: out = acc, zero padded
+    CK(cudaMemsetAsync(out, 0, out_bytes, st), "memset");
+    if (acc_bytes && acc)
+      CK(cudaMemcpyAsync(out, acc, acc_bytes < out_bytes ? acc_bytes : out_bytes,
+                         cudaMemcpyDeviceToDevice, st), "copy addend");
     return PAB_OK;
   }
-  const u64 nT = ka + kb;
   Mode md;
   if (!choose_mode(ka, kb, &md))
     return fail(PAB_ERANGE, "operands exceed the exact multi-prime convolution range");
+  const u64 nT = mul_add_words(ka, kb, kc, out_bytes);
   const Geo& geo = md.geo;
-  const Layout ly = layout_for(ka > kb ? ka : kb, geo.L, nT, nT, 1, md.np);
+  u64 kmax = ka > kb ? ka : kb;
+  kmax = kmax > kc ? kmax : kc;
+  const Layout ly = layout_for(kmax, geo.L, nT, nT, 1, md.np);
   if (workspace_bytes < ly.total) return fail(PAB_EINVAL, "workspace too small");
   int rc;
   DevState* ds;
@@ -956,7 +1038,7 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
   ConvJob job = make_job(ly, workspace, md, 1);
   job.kA = (long long)ka;
   job.kX = (long long)kb;
-  job.kD = 0;
+  job.kD = (long long)kc;
   job.nT = (long long)nT;
   // product coefficients 0 .. ca + cb - 2 (<= L - 1)
   job.nRes = (long long)(ceil_div(ka, (u64)md.cw) + ceil_div(kb, (u64)md.cw) - 1);
@@ -971,38 +1053,85 @@ int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_byt
   job.srcA = words;
   job.srcX = words + ly.in_stride;
   job.srcD = nullptr;
+  if (kc) {
+    launch_pack(acc, (long long)acc_bytes, 8ll * (long long)acc_bytes, 0, 1,
+                words + 2 * ly.in_stride, 0, (long long)kc, st);
+    job.srcD = words + 2 * ly.in_stride;
+  }
   job.src_stride = 0;
   launch_conv(job, tables_of(ds, pl), st);
   launch_carry(job, st);
-  launch_unpack(job.out_words, job.mw, 8ll * (long long)(a_bytes + b_bytes), 0, 1, out,
-                (long long)(a_bytes + b_bytes), st);
+  launch_unpack(job.out_words, job.mw, 8ll * (long long)out_bytes, 0, 1, out,
+                (long long)out_bytes, st);
   CK(cudaGetLastError(), "kernel launch");
   return PAB_OK;
 }
 
-int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes,
-                 uint8_t* out, int device) {
+static int mul_add_host(const uint8_t* acc, u64 acc_bytes, const uint8_t* a, u64 a_bytes,
+                        const uint8_t* b, u64 b_bytes, uint8_t* out, u64 out_bytes, int device) {
   CK(cudaSetDevice(device), "cudaSetDevice");
   DevState* ds;
   int rc;
   if ((rc = ensure_device(device, &ds))) return rc;
   HostCtx& h = ds->host;
   std::lock_guard<std::mutex> lk(h.mu);
-  const size_t ws = pab_mul_workspace_bytes(a_bytes, b_bytes);
+  const size_t ws = mul_add_ws(acc_bytes, a_bytes, b_bytes, out_bytes);
+  if (ws == 0) return fail(PAB_ERANGE, "operands exceed the exact multi-prime convolution range");
   const size_t io = round_up(a_bytes + 1, 256) + round_up(b_bytes + 1, 256) +
-                    round_up(a_bytes + b_bytes + 1, 256);
+                    round_up(acc_bytes + 1, 256) + round_up(out_bytes + 1, 256);
   if ((rc = host_ensure(h, ws, io))) return rc;
   uint8_t* da = h.dev_io;
   uint8_t* db = da + round_up(a_bytes + 1, 256);
-  uint8_t* dout = db + round_up(b_bytes + 1, 256);
+  uint8_t* dacc = db + round_up(b_bytes + 1, 256);
+  uint8_t* dout = dacc + round_up(acc_bytes + 1, 256);
   if (a_bytes) CK(cudaMemcpyAsync(da, a, a_bytes, cudaMemcpyHostToDevice, h.stream), "H2D a");
   if (b_bytes) CK(cudaMemcpyAsync(db, b, b_bytes, cudaMemcpyHostToDevice, h.stream), "H2D b");
-  rc = pab_mul(da, a_bytes, db, b_bytes, dout, h.ws, h.ws_bytes, h.stream);
+  if (acc_bytes)
+    CK(cudaMemcpyAsync(dacc, acc, acc_bytes, cudaMemcpyHostToDevice, h.stream), "H2D acc");
+  rc = mul_add_core(acc_bytes ? dacc : nullptr, acc_bytes, da, a_bytes, db, b_bytes, dout,
+                    out_bytes, h.ws, h.ws_bytes, h.stream);
   if (rc) return rc;
-  if (a_bytes + b_bytes)
-    CK(cudaMemcpyAsync(out, dout, a_bytes + b_bytes, cudaMemcpyDeviceToHost, h.stream), "D2H");
+  if (out_bytes) CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, h.stream), "D2H");
   CK(cudaStreamSynchronize(h.stream), "synchronize");
   return PAB_OK;
+}
+
+size_t pab_mul_workspace_bytes(uint64_t a_bytes, uint64_t b_bytes) {
+  return mul_add_ws(0, a_bytes, b_bytes, a_bytes + b_bytes);
+}
+
+int pab_mul(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes, uint8_t* out,
+            void* workspace, size_t workspace_bytes, void* stream) {
+  return mul_add_core(nullptr, 0, a, a_bytes, b, b_bytes, out, a_bytes + b_bytes, workspace,
+                      workspace_bytes, (cudaStream_t)stream);
+}
+
+int pab_mul_host(const uint8_t* a, uint64_t a_bytes, const uint8_t* b, uint64_t b_bytes,
+                 uint8_t* out, int device) {
+  return mul_add_host(nullptr, 0, a, a_bytes, b, b_bytes, out, a_bytes + b_bytes, device);
+}
+
+size_t pab_mul_add_workspace_bytes(uint64_t acc_bytes, uint64_t a_bytes, uint64_t b_bytes) {
+  const u64 ob = (a_bytes + b_bytes > acc_bytes ? a_bytes + b_bytes : acc_bytes) + 1;
+  return mul_add_ws(acc_bytes, a_bytes, b_bytes, ob);
+}
+
+int pab_mul_add(const uint8_t* acc, uint64_t acc_bytes, const uint8_t* a, uint64_t a_bytes,
+                const uint8_t* b, uint64_t b_bytes, uint8_t* out, uint64_t out_bytes,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  if (out_bytes < (a_bytes + b_bytes > acc_bytes ? a_bytes + b_bytes : acc_bytes) + 1)
+    return fail(PAB_EINVAL, "out_bytes must be >= max(a_bytes + b_bytes, acc_bytes) + 1");
+  if (acc_bytes && !acc) return fail(PAB_EINVAL, "null addend");
+  return mul_add_core(acc, acc_bytes, a, a_bytes, b, b_bytes, out, out_bytes, workspace,
+                      workspace_bytes, (cudaStream_t)stream);
+}
+
+int pab_mul_add_host(const uint8_t* acc, uint64_t acc_bytes, const uint8_t* a, uint64_t a_bytes,
+                     const uint8_t* b, uint64_t b_bytes, uint8_t* out, uint64_t out_bytes,
+                     int device) {
+  if (out_bytes < (a_bytes + b_bytes > acc_bytes ? a_bytes + b_bytes : acc_bytes) + 1)
+    return fail(PAB_EINVAL, "out_bytes must be >= max(a_bytes + b_bytes, acc_bytes) + 1");
+  return mul_add_host(acc, acc_bytes, a, a_bytes, b, b_bytes, out, out_bytes, device);
 }
 
 void pab_profile_enable(int enable) { profile_enable(enable != 0); }

@@ -175,6 +175,77 @@ __global__ void k_unpack(const u32* __restrict__ words, long long word_stride, l
   }
 }
 
+// ---------------------------------------------------------------------------
+// CPython integer digits <-> words (the drop-in's Python-int boundary)
+//
+// A CPython int holds its magnitude as 30-bit digits in 32-bit slots, least
+// significant first (sys.int_info: bits_per_digit 30).  The drop-in hands the
+// digit arrays of BitBlock.value / HashSeed.c / HashSeed.d straight to the GPU
+// and receives the key as digits, instead of int.to_bytes / int.from_bytes on
+// the host (pkg/src/modpa/pa.py:175-190 converts nothing: its ints are the data).
+
+// word j of operand y = bits [32j, 32j + 32): digits i0 = 32j / 30 and i0 + 1
+__global__ void k_digits_pack(DigitOperands ops, long long n_bits, u32* __restrict__ words,
+                              long long word_stride, long long kw) {
+  const int y = blockIdx.y;
+  const u32* __restrict__ dig = ops.d[y];
+  const long long nd = ops.nd[y];
+  u32* dst = words + (long long)y * word_stride;
+  const long long kn = (n_bits + 31) >> 5;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < kw;
+       j += (long long)gridDim.x * blockDim.x) {
+    u32 w = 0;
+    if (j < kn) {
+      const long long b0 = 32 * j;
+      const long long i0 = b0 / 30;
+      const int o = (int)(b0 - 30 * i0);  // even, 0 .. 28
+      const u32 lo = i0 < nd ? __ldg(dig + i0) : 0u;
+      const u32 hi = i0 + 1 < nd ? __ldg(dig + i0 + 1) : 0u;
+      w = (lo >> o) | (hi << (30 - o));
+      if (j == kn - 1 && (n_bits & 31)) w &= (1u << (n_bits & 31)) - 1u;
+    }
+    dst[j] = w;
+  }
+}
+
+// digit i of an m-bit LSF key = bits [30i, 30i + 30) of its words (bits >= m cleared)
+__global__ void k_digits_unpack(const u32* __restrict__ words, long long m_bits,
+                                u32* __restrict__ dig, long long nd) {
+  const long long mw = (m_bits + 31) >> 5;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nd;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b0 = 30 * i;
+    const long long w0 = b0 >> 5;
+    const int off = (int)(b0 & 31);
+    u32 v = w0 < mw ? __ldg(words + w0) >> off : 0u;
+    if (off > 2 && w0 + 1 < mw) v |= __ldg(words + w0 + 1) << (32 - off);
+    v &= 0x3FFFFFFFu;
+    const long long left = m_bits - b0;
+    if (left < 30) v = left <= 0 ? 0u : (v & ((1u << left) - 1u));
+    dig[i] = v;
+  }
+}
+
+void launch_digits_pack(const DigitOperands& ops, int nops, long long n_bits, u32* words,
+                        long long word_stride, long long kw, cudaStream_t st) {
+  const int threads = 256;
+  long long gx = (kw + threads - 1) / threads;
+  if (gx > 4096) gx = 4096;
+  if (gx < 1) gx = 1;
+  prof::Scope ps_("k_digits_pack", st);
+  k_digits_pack<<<dim3((unsigned)gx, nops), threads, 0, st>>>(ops, n_bits, words, word_stride, kw);
+}
+
+void launch_digits_unpack(const u32* words, long long m_bits, u32* dig, long long nd,
+                          cudaStream_t st) {
+  const int threads = 256;
+  long long gx = (nd + threads - 1) / threads;
+  if (gx > 4096) gx = 4096;
+  if (gx < 1) gx = 1;
+  prof::Scope ps_("k_digits_unpack", st);
+  k_digits_unpack<<<(unsigned)gx, threads, 0, st>>>(words, m_bits, dig, nd);
+}
+
 void launch_pack(const uint8_t* in, long long in_stride_bytes, long long n_bits, int msf,
                  int batch, u32* words, long long word_stride, long long kw, cudaStream_t st) {
   const int threads = 256;

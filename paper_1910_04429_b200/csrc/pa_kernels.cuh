@@ -97,6 +97,15 @@ void launch_pack(const uint8_t* in, long long in_stride_bytes, long long n_bits,
 // u32 words -> ceil(m/8) bytes per block (LSF or MSF).
 void launch_unpack(const u32* words, long long word_stride, long long m_bits, int msf, int batch,
                    uint8_t* out, long long out_stride_bytes, cudaStream_t st);
+// CPython 30-bit int digits (least significant first) <-> u32 words.
+struct DigitOperands {
+  const u32* d[3];
+  long long nd[3];  // digits present (beyond: zero)
+};
+void launch_digits_pack(const DigitOperands& ops, int nops, long long n_bits, u32* words,
+                        long long word_stride, long long kw, cudaStream_t st);
+void launch_digits_unpack(const u32* words, long long m_bits, u32* dig, long long nd,
+                          cudaStream_t st);
 // forward transforms + pointwise + inverse -> residues in buf slot A.
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st);
 // CRT + carry + mask + shift -> output.

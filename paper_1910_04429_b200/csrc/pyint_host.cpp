@@ -1,0 +1,94 @@
+// Host-side layout conversions of the drop-in boundary: CPython int digits
+// (30-bit payload in 32-bit slots, least significant first) <-> serialized
+// blocks (ceil(n/8) bytes, LSF or MSF, pkg/src/modpa/pa.py:111-132).
+//
+// The reference's import_block / export_block are int.from_bytes /
+// int.to_bytes; these do the same conversion at memory speed: four 30-bit
+// digits are exactly 15 bytes, so the loops move 120-bit groups.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/pa_b200.h"
+
+namespace {
+constexpr uint32_t kMask30 = 0x3FFFFFFFu;
+
+inline uint32_t dig_at(const uint32_t* d, uint64_t nd, uint64_t i) { return i < nd ? d[i] : 0u; }
+}  // namespace
+
+extern "C" {
+
+int pab_digits_to_bytes(const uint32_t* dig, uint64_t nd, uint8_t* out, uint64_t nbytes,
+                        int byte_order) {
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF) return PAB_EINVAL;
+  if ((nd && !dig) || (nbytes && !out)) return PAB_EINVAL;
+  const uint64_t groups = nbytes / 15;
+  uint64_t g = 0;
+  for (; g < groups; ++g) {  // 4 digits -> 15 bytes
+    const uint64_t i = 4 * g;
+    uint32_t d0, d1, d2, d3;
+    if (i + 4 <= nd) {
+      d0 = dig[i], d1 = dig[i + 1], d2 = dig[i + 2], d3 = dig[i + 3];
+    } else {
+      d0 = dig_at(dig, nd, i), d1 = dig_at(dig, nd, i + 1), d2 = dig_at(dig, nd, i + 2),
+      d3 = dig_at(dig, nd, i + 3);
+    }
+    const uint64_t lo = (uint64_t)d0 | ((uint64_t)d1 << 30) | ((uint64_t)d2 << 60);
+    const uint64_t hi = ((uint64_t)d2 >> 4) | ((uint64_t)d3 << 26);  // 56 bits
+    uint8_t* p = out + 15 * g;
+    const uint64_t up = (lo >> 56) | (hi << 8);  // bytes 7 .. 14 (one overlapping 8-byte store)
+    std::memcpy(p, &lo, 8);
+    std::memcpy(p + 7, &up, 8);
+  }
+  // tail: fewer than 15 bytes
+  uint64_t acc = 0;
+  int have = 0;
+  uint64_t i = 4 * g;
+  for (uint64_t k = 15 * g; k < nbytes; ++k) {
+    if (have < 8) {
+      acc |= (uint64_t)dig_at(dig, nd, i++) << have;
+      have += 30;
+    }
+    out[k] = (uint8_t)acc;
+    acc >>= 8;
+    have -= 8;
+  }
+  if (byte_order == PAB_ORDER_MSF) std::reverse(out, out + nbytes);
+  return PAB_OK;
+}
+
+int pab_bytes_to_digits(const uint8_t* in, uint64_t nbytes, int byte_order, uint32_t* dig,
+                        uint64_t nd) {
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF) return PAB_EINVAL;
+  if ((nbytes && !in) || (nd && !dig)) return PAB_EINVAL;
+  const bool msf = byte_order == PAB_ORDER_MSF;
+  auto byte_at = [&](uint64_t k) -> uint64_t {  // LSF byte k
+    return k < nbytes ? (msf ? in[nbytes - 1 - k] : in[k]) : 0u;
+  };
+  uint64_t i = 0;
+  if (!msf) {
+    for (; 4 * (i / 4) + 4 <= nd && 15 * (i / 4) + 15 <= nbytes; i += 4) {  // 15 bytes -> 4 digits
+      const uint8_t* p = in + 15 * (i / 4);
+      uint64_t lo, hi;
+      std::memcpy(&lo, p, 8);
+      std::memcpy(&hi, p + 7, 8);  // bytes 7 .. 14
+      hi >>= 8;
+      dig[i] = (uint32_t)lo & kMask30;
+      dig[i + 1] = (uint32_t)(lo >> 30) & kMask30;
+      dig[i + 2] = (uint32_t)((lo >> 60) | (hi << 4)) & kMask30;
+      dig[i + 3] = (uint32_t)(hi >> 26) & kMask30;
+    }
+  }
+  for (; i < nd; ++i) {  // bits [30 i, 30 i + 30) byte by byte
+    const uint64_t b0 = 30 * i;
+    const uint64_t k0 = b0 >> 3;
+    const int sh = (int)(b0 & 7);
+    uint64_t v = 0;
+    for (int q = 0; q < 5; ++q) v |= byte_at(k0 + q) << (8 * q);
+    dig[i] = (uint32_t)(v >> sh) & kMask30;
+  }
+  return PAB_OK;
+}
+
+}  // extern "C"

@@ -40,7 +40,7 @@ def test_sm100a_code_present():
 
 def test_host_only_queries():
     lib = _native.load()
-    assert lib.pab_version() == 101
+    assert lib.pab_version() == 102
     assert _native.max_bits() == 32 * ((5 * 2**22 + 1) // 2)
     # 64-bit coefficients over five primes (K' = ceil(n/64)), L = m * 2^lg >= 2K' - 1:
     # pow2 at 1e6 (32768), radix-5 at 1e7 (327680), radix-3 at 1e8 (3145728)

@@ -125,3 +125,35 @@ def test_words_round_trip():
         assert pab.from_words(pab.to_words(v, order), order).value == v
     assert pab.mod_pow2(0b1111, 2).value == 3
     assert pab.shift_right(0b1100, 2).value == 3
+
+
+def test_digit_level_int_byte_conversions():
+    # import_block / export_block over CPython digits (pab_bytes_to_digits /
+    # pab_digits_to_bytes, host code) equal int.from_bytes / int.to_bytes
+    import random
+
+    from paper_1910_04429_b200 import _pyint
+    from paper_1910_04429_b200.bignum import WordOrder
+
+    if not _pyint.supported():
+        pytest.skip("interpreter int layout not supported (byte conversions used)")
+    rng = random.Random(12)
+    for nb in list(range(0, 80)) + [255, 256, 257, 4096, 125_000, 125_001]:
+        raw = rng.randbytes(nb)
+        for msf in (False, True):
+            endian = "big" if msf else "little"
+            v = int.from_bytes(raw, endian)
+            assert _pyint.from_bytes(raw, msf) == v
+            assert _pyint.to_bytes(v, nb, msf) == raw
+            if nb:
+                assert _pyint.to_bytes(v >> 13, nb, msf) == (v >> 13).to_bytes(nb, endian)
+    for order in (WordOrder.LEAST_SIGNIFICANT_FIRST, WordOrder.MOST_SIGNIFICANT_FIRST):
+        raw = rng.randbytes(5000)
+        n = 5000 * 8 - 3
+        endian = "big" if order is WordOrder.MOST_SIGNIFICANT_FIRST else "little"
+        raw = (int.from_bytes(raw, endian) >> 3).to_bytes(5000, endian)
+        blk = pab.import_block(raw, n, order)
+        assert blk.value == int.from_bytes(raw, endian)
+        assert pab.export_block(blk, order) == raw
+    with pytest.raises(ValueError, match="beyond"):
+        pab.import_block(b"\xff" * 5000, 5000 * 8 - 3)
