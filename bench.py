@@ -2,21 +2,30 @@
 """PA hash throughput on B200 (BASELINE.json metric: input Mbps, % of roofline, bit-exact).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C3|C4|C5] [--no-extra]
+                    [--config C2|C3|C4|C5] [--no-extra] [--no-cpu] [--dry-run]
 
 A step hashes one batch of synthetic blocks (the reference's bench protocol,
 SURVEY.md §8d).  Default workload C2: 1024 blocks/rank at n=1e6, r=5e5, block
 seeds rank*1024 .. rank*1024+1023 (rank 0 = BASELINE's seeds 0..1023); weak
 scaling (blocks shard by index, no collective on the data path).
 
+`--gpus N` without torchrun re-launches itself as N ranks (torch.distributed.run,
+127.0.0.1); under torchrun WORLD_SIZE must equal N.
+
 `value`  : device-resident Mbps (inputs already in HBM), max-over-ranks time.
 `e2e`    : same metric through the public batched API from pinned host memory,
            H2D of x, c, d and D2H of the keys inside the timed region.
 `e2e_run_pa`: run_pa's scope (n <= 1e7): only the key blocks x cross PCIe; each
            block's (c, d) is expanded on the GPU (SHAKE-256) beside the hashing.
-`ratio_sweep` (--config C5): device-resident Mbps at m/n = 0.1, 0.5, 0.9.
+`roofline`: the dominant kernel against the integer-issue roofline (148 SMs x
+           128 int32 lanes/clk x the SM clock sampled under load), its executed
+           instructions from the committed ncu counts of the same batch; HBM beside.
+`n1e8`   : BASELINE configs[4] (C5): 64 blocks/rank at n=1e8, m/n 0.5 timed with its
+           own e2e, cpu_baseline and roofline; m/n 0.1 and 0.9 as `ratio_sweep`.
+`c4`     : BASELINE configs[3]: one n=1e8 block, device latency.
 `--impl reference`: the reference's CPU algorithm (the C port under oracle/,
-           all host threads, rank 0 only) on a bounded sample of the workload.
+           all host threads, rank 0 only) on the same 1024 C2 blocks per step.
+`--dry-run`: CPU only (gloo): the launcher, rank plumbing and JSON line, no kernels.
 """
 from __future__ import annotations
 
@@ -140,19 +149,42 @@ def kernel_model(n: int, r: int, blocks: int) -> dict:
     return m
 
 
-def peaks() -> dict:
+SMS = 148            # B200 (2 dies x 74)
+INT_LANES_PER_CLK = 128  # per SM: 4 SMSPs x (16-lane ALU pipe + 16-lane FMA pipe), 1 warp-instr/clk/SMSP
+
+
+def peaks(sm_mhz: float | None = None) -> dict:
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-measured copy
+    bandwidth); the integer-issue peak is the hardware dispatch limit, 148 SMs x
+    128 int32 lanes/clk at the SM clock sampled under load (else the measured max)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    hbm = None
+    mp = {}
     if os.path.exists(path):
         with open(path) as f:
-            hbm = json.load(f).get("hbm_gbs")
+            mp = json.load(f)
+    hbm = mp.get("hbm_gbs")
     src = "MEASURED_PEAKS.json" if hbm else "fallback B200_PROFILING.md"
-    int_path = os.path.join(ROOT, "profiles", "int_peak.json")
-    int_peak = None
-    if os.path.exists(int_path):
-        with open(int_path) as f:
-            int_peak = json.load(f).get("int32_tops")
-    return {"hbm_gbs": hbm or 6650.0, "hbm_src": src, "int_tops": int_peak}
+    clk = sm_mhz or mp.get("sm_max_mhz") or 1965.0
+    int_peak = SMS * INT_LANES_PER_CLK * clk * 1e6 / 1e12
+    return {"hbm_gbs": hbm or 6650.0, "hbm_src": src, "int_tops": round(int_peak, 3),
+            "sm_mhz": clk,
+            "int_src": "%d SMs x %d int32 lanes/clk x %.0f MHz (hardware issue limit; the ALU "
+                       "and FMA pipes are 64 lanes/clk/SM each)" % (SMS, INT_LANES_PER_CLK, clk)}
+
+
+def ncu_counts(workload: str | None, batch: int | None) -> dict:
+    """Per-launch ncu counters of each kernel, committed from a capture of the same
+    workload at the same blocks per launch (profiles/ncu_counts.json, written by
+    scripts/ncu_counts.py): executed warp instructions, issue-active, ALU / FMA pipe
+    utilisation and DRAM bytes."""
+    path = os.path.join(ROOT, "profiles", "ncu_counts.json")
+    if not workload or not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        rec = json.load(f).get("workloads", {}).get(workload)
+    if not rec or (batch is not None and rec.get("batch") != batch):
+        return {}
+    return rec
 
 
 # ------------------------------------------------------------------ CPU arm
@@ -163,17 +195,30 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
+PORT_NOTE = ("oracle/modpa_ssa.c: C restatement of the reference's SSA route "
+             "(pkg/src/modpa/ntt.py); its Toom-3 band (bignum.py:275-323) is served by "
+             "Karatsuba -- the same exact products, slightly different CPU cost")
+
+
 def run_reference(args, cfg) -> dict:
-    """The reference's algorithm on the host (oracle/ C port), all host threads."""
+    """The reference's algorithm on the host (oracle/ C port), all host threads, on
+    the same blocks as the GPU arm's step (all 1024 C2 blocks: ~0.8 s per step on 16
+    threads) unless that would not finish --steps K within ~3 minutes."""
     import oracle
     from paper_1910_04429_b200 import workloads
 
     n, r = cfg["n"], cfg["ms"][0]
     threads = cpu_threads()
-    # a bounded sample per step (the whole --steps K run stays within minutes)
-    per_step = max(1, min(len(cfg["seeds"]), cfg.get("ref_blocks", 4 * threads)))
-    xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"][:per_step])
-    xb, cb, db = xs.tobytes(), cs.tobytes(), ds.tobytes()
+    blocks = len(cfg["seeds"])
+    xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"])
+    probe = min(blocks, 2 * threads)
+    t0 = time.perf_counter()
+    oracle.compress_batch(xs[:probe].tobytes(), cs[:probe].tobytes(), ds[:probe].tobytes(), n, r,
+                          probe, threads)
+    per_block = (time.perf_counter() - t0) / probe
+    budget = 180.0 / max(1, args.steps + args.warmup)  # seconds per step
+    per_step = max(1, min(blocks, int(budget / max(per_block, 1e-9))))
+    xb, cb, db = (a[:per_step].tobytes() for a in (xs, cs, ds))
     for _ in range(args.warmup):
         oracle.compress_batch(xb, cb, db, n, r, per_step, threads)
     t0 = time.perf_counter()
@@ -181,9 +226,9 @@ def run_reference(args, cfg) -> dict:
         oracle.compress_batch(xb, cb, db, n, r, per_step, threads)
     dt = time.perf_counter() - t0
     mbps = args.steps * per_step * n / dt / 1e6
-    sample = f"{per_step} blocks of {cfg['name']} (n={n}, r={r}) per step"
+    sample = f"{per_step} of the {blocks} {cfg['name']} blocks (n={n}, r={r}) per step"
     return {"value": mbps, "ms_per_step": dt / args.steps * 1e3, "threads": threads,
-            "sample": sample}
+            "sample": sample, "same_config": per_step == blocks}
 
 
 def cpu_gmp_sample(cfg, xs, cs, ds, blocks: int) -> dict | None:
@@ -201,28 +246,31 @@ def cpu_gmp_sample(cfg, xs, cs, ds, blocks: int) -> dict | None:
     gmp_ref.compress_batch([a for a, _, _ in rows], [b for _, b, _ in rows],
                            [c for _, _, c in rows], n, r, threads)
     dt = time.perf_counter() - t0
-    return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps", "cores": threads,
-            "kind": "gmp (paper's method, PAPER.md:205-267)",
+    return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps",
+            "cores": min(threads, blocks), "kind": "gmp (paper's method, PAPER.md:205-267)",
             "sample": f"{blocks} blocks of {cfg['name']}, {dt:.2f}s wall"}
 
 
-def cpu_baseline_sample(cfg) -> dict:
-    """Bounded sample of the workload on the oracle port (rank 0, N=1 only)."""
+def cpu_baseline_sample(cfg, xs=None, cs=None, ds=None) -> dict:
+    """Bounded sample of the workload on the oracle port (rank 0, N=1 only), all
+    host threads (one block per thread at a time), plus the GMP context row."""
     import oracle
     from paper_1910_04429_b200 import workloads
 
     n, r = cfg["n"], cfg["ms"][0]
     threads = cpu_threads()
     blocks = min(len(cfg["seeds"]), cfg.get("cpu_blocks", 4 * threads))
-    xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"][:blocks])
+    if xs is None:
+        xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"][:blocks])
+    xs, cs, ds = xs[:blocks], cs[:blocks], ds[:blocks]
     t0 = time.perf_counter()
     out = oracle.compress_batch(xs.tobytes(), cs.tobytes(), ds.tobytes(), n, r, blocks, threads)
     dt = time.perf_counter() - t0
     gmp = cpu_gmp_sample(cfg, xs, cs, ds, blocks)
-    return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps", "cores": threads,
-            "kind": "port",
+    return {"value": round(blocks * n / dt / 1e6, 2), "unit": "Mbps",
+            "cores": min(threads, blocks), "kind": "port",
             "sample": f"{blocks} blocks of {cfg['name']} (n={n}, r={r}), {dt:.2f}s wall",
-            "context_gmp": gmp, "_out": out, "_blocks": blocks}
+            "note": PORT_NOTE, "context_gmp": gmp, "_out": out, "_blocks": blocks}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -270,64 +318,57 @@ def rank_seeds(cfg_seeds, rank: int) -> list[int]:
     return [rank * per_rank + s for s in cfg_seeds]
 
 
-def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
+def run_leg(args, cfg, rank, world, dist, steps) -> dict:
+    """One workload on this rank's GPU: device-resident timing (the contract's
+    `value`), determinism across steps, the streamed e2e leg from pinned host
+    memory, run_pa's seeded e2e (n <= 1e7) and the m/n sweep (C5)."""
     import torch
     from paper_1910_04429_b200 import workloads
     from paper_1910_04429_b200.batch import HashEngine
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as tdist
-
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        dist = tdist
     n, r = cfg["n"], cfg["ms"][0]
     per_rank = len(cfg["seeds"])
     seeds = rank_seeds(cfg["seeds"], rank)
     xs, cs, ds = workloads.batch_inputs(n, seeds)
     px, pc, pd = (torch.from_numpy(a).pin_memory() for a in (xs, cs, ds))
     dx, dc, dd = (t.cuda() for t in (px, pc, pd))
-    eng = HashEngine(n, r, max_batch=cfg.get("chunk", per_rank))
+    chunk = cfg.get("chunk", per_rank)
+    eng = HashEngine(n, r, max_batch=chunk, max_workspace=cfg.get("max_workspace", 4 << 30))
     dout = eng.hash_device(dx, dc, dd)
     torch.cuda.synchronize()
     first_out = dout.cpu()
 
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(torch.cuda.current_device())
     clk.start()
-    ms, prof = time_device(eng, dx, dc, dd, dout, args.steps, args.warmup, dist)
-    ms_step = max_over_ranks(ms / args.steps, dist)
+    ms, prof = time_device(eng, dx, dc, dd, dout, steps, args.warmup, dist)
+    ms_step = max_over_ranks(ms / steps, dist)
     bits_step = world * per_rank * n
     value = bits_step / (ms_step * 1e-3) / 1e6
-
-    # determinism across the timed steps (same inputs -> same keys)
     assert torch.equal(dout.cpu(), first_out), "keys changed across steps"
 
-    # end-to-end through the public batched API from pinned host memory
+    # end to end through the public batched API from pinned host memory
     hout = torch.empty((per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
     for _ in range(max(1, args.warmup)):
         eng.hash_host(px, pc, pd, hout, streams=3, chunk=cfg.get("e2e_chunk"))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    t0 = time.perf_counter()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for i in range(args.steps):  # streamed: each step's head overlaps the previous tail
+    for i in range(steps):  # streamed: each step's head overlaps the previous tail
         eng.hash_host(px, pc, pd, hout, streams=3, chunk=cfg.get("e2e_chunk"),
                       join_in=i == 0, join_out=False)
     eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
     clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
     assert torch.equal(hout, first_out), "e2e keys differ from device-resident keys"
     # the PCIe bound of that leg: the same pinned H2D + D2H bytes, copies only
-    # (H2D and D2H overlapped on two streams, as hash_host overlaps them)
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = max(2, min(args.steps, 10))
+    reps = max(2, min(steps, 10))
     torch.cuda.synchronize()
     c0.record(st)
     s_in.wait_stream(st)
@@ -349,38 +390,35 @@ def run_ours(args, cfg, rank, local_rank, world) -> dict | None:
            "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(e2e_ms, 4),
            "copy_only_ms_per_step": round(copy_ms, 4),
            "h2d_gbps": round(3 * per_rank * eng.nbytes / (e2e_ms * 1e-3) / 1e9, 1),
-           "frac_of_copy_bound": round(copy_ms / e2e_ms, 4)}
+           "frac_of_copy_bound": round(copy_ms / e2e_ms, 4),
+           "scope": "HashEngine.hash_host: pinned x, c, d -> GPU, keys -> pinned host, "
+                    "consecutive steps streamed"}
 
-    e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) \
+    e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) \
         if n <= 10_000_000 else None
 
-    # C5's compression-ratio sweep (BASELINE configs[4]: m/n in {0.1, 0.5, 0.9}),
-    # device-resident, same blocks; the output length only changes the carry's writes
     sweep = None
-    if len(cfg["ms"]) > 1:
+    if len(cfg["ms"]) > 1:  # C5 (BASELINE configs[4]): m/n in {0.1, 0.5, 0.9}, same blocks
         sweep = []
-        for rr in cfg["ms"]:
-            e_r = HashEngine(n, rr, max_batch=cfg.get("chunk", per_rank))
+        for rr in cfg["ms"][1:]:
+            e_r = HashEngine(n, rr, max_batch=chunk, max_workspace=cfg.get("max_workspace", 4 << 30))
             o_r = e_r.hash_device(dx, dc, dd)
-            k = max(3, min(args.steps, 10))
-            ms_r, _ = time_device(e_r, dx, dc, dd, o_r, k, max(3, args.warmup // 2), dist,
-                                  profile=False)
+            k = max(3, min(steps, 10))
+            ms_r, _ = time_device(e_r, dx, dc, dd, o_r, k, 3, dist, profile=False)
             ms_r = max_over_ranks(ms_r / k, dist)
-            sr = step_roofline(n, rr, per_rank, ms_r)
+            sr = step_roofline(n, rr, per_rank, ms_r, clocks.get("sm_mhz"))
             sweep.append({"r": rr, "ratio": round(rr / n, 3),
                           "value": round(bits_step / (ms_r * 1e-3) / 1e6, 1),
                           "ms_per_step": round(ms_r, 4), "steps": k,
-                          "step_roofline_frac": sr["frac"] if sr else None})
+                          "step_roofline_frac": sr["frac"]})
             del e_r, o_r
-
-    res = {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
-           "e2e_seeded": e2e_seeded, "ratio_sweep": sweep,
-           "out": first_out, "per_rank": per_rank, "n": n, "r": r, "eng": eng,
-           "dist": dist, "seeds": seeds}
-    return res
+    return {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
+            "e2e_seeded": e2e_seeded, "ratio_sweep": sweep, "out": first_out,
+            "per_rank": per_rank, "n": n, "r": r, "eng": eng, "seeds": seeds, "steps": steps,
+            "inputs": (xs, cs, ds), "chunk": eng.chunk}
 
 
-def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) -> dict:
+def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict:
     """run_pa's scope end to end (pkg/src/modpa/bench.py:256-262): the key blocks
     from pinned host memory, block i hashed with gen_seed(n, derive_block_seed(0, i))
     expanded on the GPU (HashEngine.hash_seeded_host), keys back to the host.  Only
@@ -398,12 +436,12 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) -> dict:
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for i in range(args.steps):
+    for i in range(steps):
         eng.hash_seeded_host(px, 0, first, hout, streams=3, join_in=i == 0, join_out=False)
     eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist)
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
     # spot check: two blocks against host-derived seeds through the device path
     nb = eng.nbytes
     idx = [0, per_rank - 1]
@@ -423,82 +461,98 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist) -> dict:
             "ms_per_step": round(ms, 4)}
 
 
-def ncu_traffic(workload: str | None, batch: int | None = None) -> dict:
-    """Per-launch DRAM bytes of each kernel from the committed ncu capture of this
-    workload, if it was captured at the same blocks per launch."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not workload or not os.path.exists(path):
-        return {}
-    with open(path) as f:
-        rec = json.load(f).get("workloads", {}).get(workload, {})
-    if batch is not None and rec.get("batch") not in (None, batch):
-        return {}
-    return {k: v for k, v in rec.items() if k != "batch"}
+def roofline_obj(prof: dict, n: int, r: int, blocks: int, workload: str | None,
+                 sm_mhz: float | None) -> tuple[dict, dict]:
+    """The contract's `roofline` for the dominant kernel plus a per-kernel table.
 
-
-def roofline_obj(prof: dict, steps: int, n: int, r: int, blocks: int,
-                 workload: str | None = None) -> tuple[dict, dict]:
+    The NTT kernels are integer-pipe bound (HBM < 0.5), so `bound` is "int":
+    achieved = executed thread-instructions per launch (ncu smsp__inst_executed x 32,
+    same workload and batch) / the live CUDA-event launch time, peak = the hardware
+    issue limit at the sampled clock.  frac is therefore the kernel's issue-slot
+    occupancy and should agree with ncu's issue-active.  The algorithmic-op rate
+    (DESIGN.md §4 cost model) and the HBM fraction of the algorithmic bytes sit beside.
+    """
     model = kernel_model(n, r, blocks)
-    pk = peaks()
-    traffic = ncu_traffic(workload, blocks)
+    pk = peaks(sm_mhz)
+    cnt = ncu_counts(workload, blocks)
+    kcnt = cnt.get("kernels", {})
     total = sum(v[1] for v in prof.values()) or 1.0
     kernels = {}
-    for name, (cnt, ms) in prof.items():
-        avg_ms = ms / max(cnt, 1)
+    for name, (c, ms) in prof.items():
+        avg_s = ms / max(c, 1) * 1e-3
         mdl = model.get(name, {"bytes": 0, "ops": 0})
-        kernels[name] = {"launches": cnt, "avg_ms": round(avg_ms, 4),
-                         "share": round(ms / total, 4),
-                         "GBps": round(mdl["bytes"] / (avg_ms * 1e-3) / 1e9, 1),
-                         "Tops": round(mdl["ops"] / (avg_ms * 1e-3) / 1e12, 2)}
-    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
-    roof = None
-    if dom:
-        cnt, ms = prof[dom]
-        avg_s = ms / max(cnt, 1) * 1e-3
-        mdl = model[dom]
-        ach = mdl["bytes"] / avg_s / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
-                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 4),
-                "traffic": traffic.get(dom), "peak_src": pk["hbm_src"],
-                "algorithmic_bytes_per_launch": mdl["bytes"]}
-        if pk["int_tops"]:
-            ach_ops = mdl["ops"] / avg_s / 1e12
-            roof["int"] = {"achieved": round(ach_ops, 2), "peak": pk["int_tops"],
-                           "unit": "Tops/s", "frac": round(ach_ops / pk["int_tops"], 4),
-                           "ops_per_launch": mdl["ops"]}
-            if ach_ops / pk["int_tops"] > ach / pk["hbm_gbs"]:
-                roof["binding"] = "int"
+        k = {"launches": c, "avg_ms": round(avg_s * 1e3, 4), "share": round(ms / total, 4),
+             "GBps": round(mdl["bytes"] / avg_s / 1e9, 1),
+             "alg_Tops": round(mdl["ops"] / avg_s / 1e12, 2)}
+        if name in kcnt:
+            k["issue_frac"] = round(kcnt[name]["inst"] * 32 / avg_s / 1e12 / pk["int_tops"], 4)
+        kernels[name] = k
+    if not prof:
+        return None, kernels
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0]
+    c, ms = prof[dom]
+    avg_s = ms / max(c, 1) * 1e-3
+    mdl = model.get(dom, {"bytes": 0, "ops": 0})
+    gbps = mdl["bytes"] / avg_s / 1e9
+    hbm = {"achieved": round(gbps, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+           "frac": round(gbps / pk["hbm_gbs"], 4), "peak_src": pk["hbm_src"],
+           "algorithmic_bytes_per_launch": mdl["bytes"]}
+    alg = {"ops_per_launch": mdl["ops"], "achieved": round(mdl["ops"] / avg_s / 1e12, 3),
+           "unit": "Tops/s", "frac_of_issue_peak": round(mdl["ops"] / avg_s / 1e12 / pk["int_tops"], 4),
+           "model": "DESIGN.md §4: 7 ops per radix-2 butterfly, 6 per Montgomery product, "
+                    "8 per four-step twiddle, CRT 85 (5 primes) / 35 (3) per coefficient"}
+    kc = kcnt.get(dom)
+    if kc:
+        ops = kc["inst"] * 32
+        ach = ops / avg_s / 1e12
+        roof = {"bound": "int", "kernel": dom, "achieved": round(ach, 3), "peak": pk["int_tops"],
+                "unit": "Tops/s", "frac": round(ach / pk["int_tops"], 4),
+                "traffic": kc.get("dram_bytes"), "peak_src": pk["int_src"],
+                "ops_per_launch": ops,
+                "ops_src": "smsp__inst_executed.sum x 32 of %s (profiles/ncu_counts.json: %s, "
+                           "%d blocks/launch)" % (dom, workload, blocks),
+                "ncu": {x: kc.get(x) for x in ("issue_active", "pipe_alu", "pipe_fma",
+                                                "duration_ms", "sm_mhz")},
+                "hbm": hbm, "algorithmic": alg}
+    else:  # no matching capture committed: report the algorithmic HBM fraction only
+        roof = dict(hbm, bound="hbm", kernel=dom, traffic=None, algorithmic=alg,
+                    note="no ncu counts for this workload/batch: int fraction unavailable")
     return roof, kernels
 
 
-def step_roofline(n: int, r: int, blocks: int, ms_step: float) -> dict | None:
-    """North-star roofline of a whole step: the slower of (canonical int ops at the
-    measured int peak) and (algorithmic HBM bytes at the measured copy bandwidth),
-    summed over the step's kernels, vs the measured step time."""
-    pk = peaks()
-    if not pk["int_tops"]:
-        return None
+def step_roofline(n: int, r: int, blocks: int, ms_step: float, sm_mhz: float | None,
+                  workload: str | None = None, chunk: int | None = None) -> dict:
+    """North-star roofline of a whole step: the slower of (the step's algorithmic int
+    ops at the hardware issue peak) and (its algorithmic HBM bytes at the measured
+    copy bandwidth), vs the measured step time; plus, where the ncu counts of this
+    batch are committed, the executed instructions at the same peak (issue_frac)."""
+    pk = peaks(sm_mhz)
     model = kernel_model(n, r, blocks)
-    ops = sum(v["ops"] for k, v in model.items() if k not in ("k_pack", "k_unpack"))
-    byts = sum(v["bytes"] for k, v in model.items() if k not in ("k_pack", "k_unpack"))
+    ops = sum(v["ops"] for v in model.values())
+    byts = sum(v["bytes"] for v in model.values())
     t_int = ops / (pk["int_tops"] * 1e12) * 1e3
     t_hbm = byts / (pk["hbm_gbs"] * 1e9) * 1e3
     t_roof = max(t_int, t_hbm)
-    return {"t_int_ms": round(t_int, 4), "t_hbm_ms": round(t_hbm, 4), "t_roof_ms": round(t_roof, 4),
-            "measured_ms": round(ms_step, 4), "frac": round(t_roof / ms_step, 4),
-            "bound": "int" if t_int >= t_hbm else "hbm",
-            "roofline_mbps": round(blocks * n / t_roof / 1e3, 1)}
+    out = {"t_int_ms": round(t_int, 4), "t_hbm_ms": round(t_hbm, 4), "t_roof_ms": round(t_roof, 4),
+           "measured_ms": round(ms_step, 4), "frac": round(t_roof / ms_step, 4),
+           "bound": "int" if t_int >= t_hbm else "hbm",
+           "roofline_mbps": round(blocks * n / t_roof / 1e3, 1),
+           "peak": {"int_tops": pk["int_tops"], "hbm_gbs": pk["hbm_gbs"]}}
+    cnt = ncu_counts(workload, chunk or blocks).get("kernels", {})
+    if cnt:
+        launches = max(1, blocks // (chunk or blocks))
+        inst = sum(v["inst"] for v in cnt.values()) * 32 * launches
+        out["issue_frac"] = round(inst / (pk["int_tops"] * 1e12) * 1e3 / ms_step, 4)
+    return out
 
 
-def baseline_roofline(n: int, r: int, blocks: int, ms_step: float) -> dict | None:
-    """The BASELINE.md §4 roofline: the canonical G16 design (Goldilocks prime,
-    16-bit coefficients, 2 HBM passes per NTT) at the measured int peak and HBM
-    bandwidth -- the north star's "NTT roofline" as frozen before optimising.
-    This design does fewer ops than G16, so its frac can exceed 1; step_roofline
-    is the same ratio against this design's own op count."""
-    pk = peaks()
-    if not pk["int_tops"]:
-        return None
+def baseline_roofline(n: int, r: int, blocks: int, ms_step: float, sm_mhz: float | None) -> dict:
+    """BASELINE.md §4's frozen yardstick: the canonical G16 design (Goldilocks prime,
+    16-bit coefficients, 26 ops per radix-2 butterfly, 2 HBM passes per NTT) at the
+    hardware int issue peak and the measured HBM bandwidth.  This design does far
+    fewer ops per bit (5 primes x 64-bit coefficients, 7-op Shoup butterflies), so
+    its frac exceeds 1 without any skipped work."""
+    pk = peaks(sm_mhz)
     K = -(-n // 16)
     L = 1 << (2 * K - 2).bit_length()
     lg = L.bit_length() - 1
@@ -536,6 +590,102 @@ def dropin_timing(n: int, r: int, calls: int = 10) -> dict:
                      "int<->bytes and host<->device copies (median of %d)" % (n, calls)}
 
 
+def leg_line(args, cfg, res, world, cpu=None) -> dict:
+    """The JSON fields of one measured workload."""
+    n, r, per_rank = res["n"], res["r"], res["per_rank"]
+    sm = res["clocks"].get("sm_mhz")
+    roof, kernels = roofline_obj(res["prof"], n, r, res["chunk"], cfg["name"], sm)
+    return {
+        "value": round(res["value"], 1), "unit": "Mbps", "ms_per_step": round(res["ms_step"], 4),
+        "steps": res["steps"],
+        "config": {"workload": cfg["name"], "n": n, "r": r, "blocks_per_rank": per_rank,
+                   "blocks_per_launch": res["chunk"],
+                   "block_seeds": "rank*%d + 0..%d" % (per_rank, per_rank - 1),
+                   "parallelism": f"blocks sharded by index over {world} GPU(s), no collective",
+                   "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
+                         % (3 * per_rank * ((n + 7) // 8) / 1e6)},
+        "e2e": res["e2e"], "e2e_run_pa": res["e2e_seeded"],
+        "gpu_launches": sum(v[0] for v in res["prof"].values()),
+        "roofline": roof,
+        "step_roofline": step_roofline(n, r, per_rank, res["ms_step"], sm, cfg["name"],
+                                       res["chunk"]),
+        "baseline_roofline": baseline_roofline(n, r, per_rank, res["ms_step"], sm),
+        "kernels": kernels, "clocks": res["clocks"], "cpu_baseline": cpu,
+        "ratio_sweep": res["ratio_sweep"],
+    }
+
+
+def cpu_leg(cfg, res) -> dict:
+    """cpu_baseline of a leg on its own blocks, with the bit-exactness check."""
+    xs, cs, ds = res["inputs"]
+    cpu = cpu_baseline_sample(cfg, xs, cs, ds)
+    k = cpu.pop("_blocks")
+    cpu_out = cpu.pop("_out")
+    cpu["bit_exact_vs_gpu"] = cpu_out == res["out"][:k].numpy().tobytes()
+    return cpu
+
+
+def c4_leg(args, dist) -> dict:
+    """BASELINE configs[3]: one n=1e8 block (seed 7), r=5e7 -- device latency of the
+    largest single product, per-kernel times and the drop-in compress call."""
+    import torch
+    from paper_1910_04429_b200 import workloads
+    from paper_1910_04429_b200.batch import HashEngine
+
+    cfg = workloads.CONFIGS["C4"]
+    n, r = cfg["n"], cfg["ms"][0]
+    xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"])
+    dx, dc, dd = (torch.from_numpy(a).cuda() for a in (xs, cs, ds))
+    eng = HashEngine(n, r, max_batch=1)
+    dout = eng.hash_device(dx, dc, dd)
+    steps = max(3, min(args.steps, 20))
+    ms, prof = time_device(eng, dx, dc, dd, dout, steps, 3, dist)
+    ms = max_over_ranks(ms / steps, dist)
+    roof, kernels = roofline_obj(prof, n, r, 1, "C4", None)
+    out = {"workload": "C4: 1 block, n=1e8, r=5e7, seed 7", "ms_per_block": round(ms, 4),
+           "value": round(n / (ms * 1e-3) / 1e6, 1), "unit": "Mbps", "steps": steps,
+           "kernels": kernels, "roofline": roof}
+    if not args.no_extra and (not dist or dist.get_rank() == 0):
+        out["dropin"] = dropin_timing(n, r, calls=3)
+    return out
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: run this script as N ranks (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args, rank, world) -> None:
+    """CPU-only check of the multi-rank plumbing (gloo): barrier, max-over-ranks,
+    block shards, one JSON line from rank 0.  Measures nothing."""
+    import torch.distributed as tdist
+
+    dist = None
+    if world > 1:
+        tdist.init_process_group("gloo")
+        dist = tdist
+        dist.barrier()
+    from paper_1910_04429_b200.workloads import CONFIGS
+
+    seeds = rank_seeds(CONFIGS[args.config]["seeds"], rank)
+    t = max_over_ranks(float(rank + 1), dist)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "value": None, "unit": "Mbps",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "max_over_ranks_check": t, "rank0_seeds": [seeds[0], seeds[-1]],
+                          "config": {"workload": args.config}}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -543,31 +693,38 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
-    ap.add_argument("--no-extra", action="store_true", help="skip the n=1e8 side measurement")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the n=1e8 legs and drop-in timing")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    rank, local_rank, world = dist_env()
+    under_launcher = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not under_launcher and args.impl == "ours":
+        sys.exit(relaunch(args))
+    if under_launcher and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return dry_run(args, rank, world)
 
     from paper_1910_04429_b200.workloads import CONFIGS
 
     cfg = dict(CONFIGS[args.config])
     cfg["name"] = args.config
     if args.config in ("C4", "C5"):
-        cfg["cpu_blocks"] = 2
-        cfg["ref_blocks"] = 1
-        cfg["chunk"] = 16  # one launch per 16-block step (2.0 GiB workspace; 8-block launches 2% slower)
+        cfg["cpu_blocks"] = cpu_threads()
+        cfg["chunk"] = 64            # one launch per 64-block step (8 GiB workspace)
+        cfg["max_workspace"] = 9 << 30
         cfg["e2e_chunk"] = 2
         if args.config == "C5":
-            cfg["seeds"] = tuple(range(16))  # 16 blocks/rank per step (1.6 Gbit)
-            cfg["ms"] = (50_000_000, 10_000_000, 90_000_000)  # main line at m/n = 0.5, then the sweep
+            cfg["ms"] = (50_000_000, 10_000_000, 90_000_000)  # main line m/n = 0.5, then the sweep
     elif args.config == "C3":
         cfg["cpu_blocks"] = 16
         cfg["e2e_chunk"] = 8
     else:
         cfg["e2e_chunk"] = 128
         cfg["cpu_blocks"] = 1024
-    rank, local_rank, world = dist_env()
 
     if args.impl == "reference":
         if rank != 0:
@@ -579,88 +736,57 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "u32", "data": "synthetic (SHAKE-256 seeded blocks, reference bench protocol)",
                 "config": {"workload": cfg["name"], "n": cfg["n"], "r": cfg["ms"][0],
-                           "blocks_per_step": ref["sample"]},
+                           "blocks_per_step": ref["sample"], "same_config": ref["same_config"]},
                 "cpu_baseline": {"value": round(ref["value"], 2), "unit": "Mbps",
                                  "cores": ref["threads"], "kind": "port",
-                                 "sample": ref["sample"]},
+                                 "sample": ref["sample"], "note": PORT_NOTE},
                 "e2e": {"value": round(ref["value"], 2), "unit": "Mbps",
                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
-    res = run_ours(args, cfg, rank, local_rank, world)
-    n, r, per_rank = res["n"], res["r"], res["per_rank"]
-    roof, kernels = roofline_obj(res["prof"], args.steps, n, r, res["eng"].chunk,
-                                 workload=cfg["name"])
-    step_roof = step_roofline(n, r, per_rank, res["ms_step"])
-    base_roof = baseline_roofline(n, r, per_rank, res["ms_step"])
-    launches = sum(v[0] for v in res["prof"].values())
-    dropin = dropin_timing(n, r) if rank == 0 and world == 1 and not args.no_extra else None
+    import torch
 
-    extra = {}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(cfg)
-        k = cpu.pop("_blocks")
-        cpu_out = cpu.pop("_out")
-        rb = (r + 7) // 8
-        cpu["bit_exact_vs_gpu"] = cpu_out == res["out"][:k].numpy().tobytes()
-    if rank == 0 and not args.no_extra and args.config == "C2":
-        extra = side_1e8(args, res["dist"])
-    elif res["dist"] and not args.no_extra and args.config == "C2":
-        side_1e8(args, res["dist"])
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    solo = rank == 0 and world == 1
+
+    res = run_leg(args, cfg, rank, world, dist, args.steps)
+    cpu = cpu_leg(cfg, res) if solo and not args.no_cpu else None
+    line = leg_line(args, cfg, res, world, cpu)
+    line["dropin"] = dropin_timing(res["n"], res["r"]) if solo and not args.no_extra else None
+    eng = res.pop("eng")
+    del res, eng
+    torch.cuda.empty_cache()
+
+    side = {}
+    if not args.no_extra and args.config == "C2":
+        c5 = dict(CONFIGS["C5"], name="C5", ms=(50_000_000, 10_000_000, 90_000_000),
+                  chunk=64, max_workspace=9 << 30, e2e_chunk=2, cpu_blocks=cpu_threads())
+        r5 = run_leg(args, c5, rank, world, dist, max(3, min(args.steps, 10)))
+        cpu5 = cpu_leg(c5, r5) if solo and not args.no_cpu else None
+        side["n1e8"] = leg_line(args, c5, r5, world, cpu5)
+        del r5
+        torch.cuda.empty_cache()
+        side["c4"] = c4_leg(args, dist)
 
     if rank == 0:
-        pk = peaks()
-        line = {
-            "metric": METRIC, "value": round(res["value"], 1), "unit": "Mbps",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(res["ms_step"], 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (SHAKE-256 seeded blocks, reference bench protocol)",
-            "config": {"workload": cfg["name"], "n": n, "r": r, "blocks_per_rank": per_rank,
-                       "block_seeds": "rank*%d + 0..%d" % (per_rank, per_rank - 1),
-                       "parallelism": f"blocks sharded by index over {world} GPU(s), no collective",
-                       "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
-                             % (3 * per_rank * ((n + 7) // 8) / 1e6)},
-            "e2e": res["e2e"], "e2e_run_pa": res["e2e_seeded"], "gpu_launches": launches,
-            "roofline": roof,
-            "step_roofline": step_roof, "baseline_roofline": base_roof, "dropin": dropin,
-            "kernels": kernels, "clocks": res["clocks"], "cpu_baseline": cpu,
-        }
-        if extra:
-            line["n1e8"] = extra
-        if res.get("ratio_sweep"):
-            line["ratio_sweep"] = res["ratio_sweep"]
-        print(json.dumps(line), flush=True)
-    if res["dist"]:
-        res["dist"].destroy_process_group()
-
-
-def side_1e8(args, dist) -> dict:
-    """Secondary metric at n=1e8 (BASELINE metric is quoted at 1e6 and 1e8):
-    4 blocks of C5 at ratio 0.5 per step, device-resident, few steps."""
-    import torch
-    from paper_1910_04429_b200 import workloads
-    from paper_1910_04429_b200.batch import HashEngine
-
-    n, r, B = 100_000_000, 50_000_000, 4
-    rank = dist.get_rank() if dist else 0
-    xs, cs, ds = workloads.batch_inputs(n, [rank * B + i for i in range(B)])
-    dx, dc, dd = (torch.from_numpy(a).cuda() for a in (xs, cs, ds))
-    del xs, cs, ds
-    eng = HashEngine(n, r, max_batch=B)
-    dout = eng.hash_device(dx, dc, dd)
-    steps = max(2, min(args.steps, 5))
-    ms, prof = time_device(eng, dx, dc, dd, dout, steps, 3, dist)
-    ms_step = max_over_ranks(ms / steps, dist)
-    world = dist.get_world_size() if dist else 1
-    roof, kernels = roofline_obj(prof, steps, n, r, B)
-    return {"workload": "C5 subset: %d blocks/rank, n=1e8, r=5e7" % B,
-            "value": round(world * B * n / (ms_step * 1e-3) / 1e6, 1), "unit": "Mbps",
-            "ms_per_step": round(ms_step, 3), "roofline": roof,
-            "step_roofline": step_roofline(n, r, B, ms_step),
-            "baseline_roofline": baseline_roofline(n, r, B, ms_step), "kernels": kernels}
+        out = {"metric": METRIC, "value": line.pop("value"), "unit": "Mbps", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": line.pop("ms_per_step"), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+               "data": "synthetic (SHAKE-256 seeded blocks, reference bench protocol)"}
+        line.pop("steps")
+        out.update(line)
+        out.update(side)
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

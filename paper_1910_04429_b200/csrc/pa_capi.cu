@@ -164,7 +164,8 @@ struct HostCtx {  // cached buffers for the host-pointer entry points
   size_t ws_bytes = 0;
   uint8_t* dev_io = nullptr;
   size_t dev_io_bytes = 0;
-  uint8_t* pinned = nullptr;      // pinned staging of the Python-int digit path
+  uint8_t* pinned = nullptr;      // pinned, mapped staging of the Python-int digit path
+  uint8_t* pinned_dev = nullptr;
   size_t pinned_bytes = 0;
   std::mutex mu;
 };
@@ -763,20 +764,20 @@ int pab_hash_digits(const uint32_t* x, uint64_t x_nd, const uint32_t* c, uint64_
   const u64 rbytes = ceil_div(r_bits, 8), out_stride = round_up(rbytes, 16);
   const u64 dig_in = 4 * (xn + cn + dn), dig_out = 4 * out_nd;
   const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, 1);
-  const size_t io_bytes = 3 * in_stride + round_up(dig_in, 256) + out_stride + round_up(dig_out, 256);
+  const size_t io_bytes = 3 * in_stride + round_up(dig_in, 256) + out_stride;
   if ((rc = host_ensure(h, ws_bytes, io_bytes))) return rc;
   const size_t pin_bytes = round_up(dig_in, 256) + round_up(dig_out, 256);
   if (h.pinned_bytes < pin_bytes) {
     if (h.pinned) cudaFreeHost(h.pinned);
     h.pinned = nullptr;
     h.pinned_bytes = 0;
-    CK(cudaHostAlloc((void**)&h.pinned, pin_bytes, cudaHostAllocDefault), "pinned alloc");
+    CK(cudaHostAlloc((void**)&h.pinned, pin_bytes, cudaHostAllocMapped), "pinned alloc");
+    CK(cudaHostGetDevicePointer((void**)&h.pinned_dev, h.pinned, 0), "mapped pointer");
     h.pinned_bytes = pin_bytes;
   }
   uint8_t* words = h.dev_io;                        // x, c, d rows
   uint8_t* ddig = words + 3 * in_stride;            // input digits
   uint8_t* dout = ddig + round_up(dig_in, 256);     // key bytes (LSF, 16-byte padded)
-  uint8_t* dodig = dout + out_stride;               // key digits
   uint8_t* pin_out = h.pinned + round_up(dig_in, 256);
   std::memcpy(h.pinned, x, 4 * xn);
   std::memcpy(h.pinned + 4 * xn, c, 4 * cn);
@@ -794,10 +795,10 @@ int pab_hash_digits(const uint32_t* x, uint64_t x_nd, const uint32_t* c, uint64_
   rc = pab_hash_batch(words, words + in_stride, words + 2 * in_stride, in_stride, n_bits, r_bits,
                       1, PAB_ORDER_LSF, dout, out_stride, h.ws, h.ws_bytes, h.stream);
   if (rc) return rc;
-  launch_digits_unpack((const u32*)dout, (long long)r_bits, (u32*)dodig, (long long)out_nd,
-                       h.stream);
+  // the key digits go straight to mapped host memory (posted PCIe writes, no D2H copy)
+  launch_digits_unpack((const u32*)dout, (long long)r_bits,
+                       (u32*)(h.pinned_dev + round_up(dig_in, 256)), (long long)out_nd, h.stream);
   CK(cudaGetLastError(), "kernel launch");
-  CK(cudaMemcpyAsync(pin_out, dodig, dig_out, cudaMemcpyDeviceToHost, h.stream), "D2H");
   CK(cudaStreamSynchronize(h.stream), "synchronize");
   std::memcpy(out, pin_out, dig_out);
   return PAB_OK;

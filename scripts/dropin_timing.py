@@ -1,22 +1,28 @@
-"""Per-call timing of the drop-in compress at tiny and 1e6 sizes (development aid)."""
+"""Per-call timing of the drop-in pieces at 1e6 bits by compression ratio (development aid)."""
 import sys, time
 sys.path.insert(0, ".")
 import paper_1910_04429_b200 as pab
 
-for alpha in (7, 64, 2048, 100_000, 1_000_000):
-    x = pab.BitBlock(pab.pa._expand(1, b"x", alpha), alpha)
-    s = pab.gen_seed(alpha, 5)
-    r = max(1, alpha // 2)
-    pab.compress(x, s, r)
-    k = 20000 if alpha <= 2048 else 200
-    t0 = time.perf_counter()
+n = 1_000_000
+x = pab.BitBlock(pab.pa._expand(1, b"x", n), n)
+raw = pab.export_block(x)
+s = pab.gen_seed(n, 5)
+
+
+def best(f, k=200):
+    f()
+    b = 1e9
     for _ in range(k):
-        pab.compress(x, s, r)
-    dt = (time.perf_counter() - t0) / k
-    for ratio in (0.125, 0.9):
-        rr = max(1, int(alpha * ratio))
-        t1 = time.perf_counter()
-        for _ in range(min(k, 200)):
-            pab.compress(x, s, rr)
-        print(f"alpha={alpha} r/n={ratio}: {(time.perf_counter() - t1) / min(k, 200) * 1e6:.1f} us")
-    print(f"alpha={alpha}: {dt * 1e6:.1f} us per compress", flush=True)
+        t0 = time.perf_counter()
+        f()
+        b = min(b, time.perf_counter() - t0)
+    return b * 1e6
+
+
+print("import_block", round(best(lambda: pab.import_block(raw, n)), 1), "us")
+for ratio in (0.125, 0.5, 0.9):
+    r = int(n * ratio)
+    out = pab.compress(x, s, r)
+    print(ratio, "compress", round(best(lambda: pab.compress(x, s, r)), 1),
+          "export", round(best(lambda: pab.export_block(out)), 1),
+          "round", round(best(lambda: pab.export_block(pab.pa_round(pab.import_block(raw, n), pab.PAParams(n=n, r=r), s, enforce=False))), 1))

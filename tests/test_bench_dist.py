@@ -47,3 +47,33 @@ def test_kernel_model_positive():
     if m:
         assert set(m) >= {"k_col_fwd", "k_row", "k_col_inv", "k_carry"}
         assert all(v["bytes"] > 0 for k, v in m.items() if k.startswith("k_"))
+
+
+def test_gpus_flag_self_launches_ranks():
+    # `python bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    # (torch.distributed.run on 127.0.0.1); --dry-run keeps it on CPU/gloo
+    import json
+    import subprocess
+    import sys
+
+    res = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2",
+                          "--dry-run", "--steps", "3"], capture_output=True, text=True,
+                         timeout=240, cwd=bench.ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert d["max_over_ranks_check"] == 2.0  # rank 1 reported 2.0, rank 0 1.0
+    assert d["rank0_seeds"] == [0, 1023]
+
+
+def test_world_size_must_match_gpus():
+    import subprocess
+    import sys
+
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "1",
+                          "--dry-run"], capture_output=True, text=True, timeout=120, env=env,
+                         cwd=bench.ROOT)
+    assert res.returncode != 0 and "WORLD_SIZE=2" in res.stderr
