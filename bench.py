@@ -512,7 +512,7 @@ def roofline_obj(prof: dict, n: int, r: int, blocks: int, workload: str | None,
                 "ops_src": "smsp__inst_executed.sum x 32 of %s (profiles/ncu_counts.json: %s, "
                            "%d blocks/launch)" % (dom, workload, blocks),
                 "ncu": {x: kc.get(x) for x in ("issue_active", "pipe_alu", "pipe_fma",
-                                                "duration_ms", "sm_mhz")},
+                                                "pipe_fmaheavy", "duration_ms", "sm_mhz")},
                 "hbm": hbm, "algorithmic": alg}
     else:  # no matching capture committed: report the algorithmic HBM fraction only
         roof = dict(hbm, bound="hbm", kernel=dom, traffic=None, algorithmic=alg,
@@ -714,8 +714,8 @@ def main():
     cfg["name"] = args.config
     if args.config in ("C4", "C5"):
         cfg["cpu_blocks"] = cpu_threads()
-        cfg["chunk"] = 64            # one launch per 64-block step (8 GiB workspace)
-        cfg["max_workspace"] = 9 << 30
+        cfg["chunk"] = 64            # one launch per 64-block step (10.5 GiB workspace)
+        cfg["max_workspace"] = 12 << 30
         cfg["e2e_chunk"] = 2
         if args.config == "C5":
             cfg["ms"] = (50_000_000, 10_000_000, 90_000_000)  # main line m/n = 0.5, then the sweep
@@ -767,7 +767,7 @@ def main():
     side = {}
     if not args.no_extra and args.config == "C2":
         c5 = dict(CONFIGS["C5"], name="C5", ms=(50_000_000, 10_000_000, 90_000_000),
-                  chunk=64, max_workspace=9 << 30, e2e_chunk=2, cpu_blocks=cpu_threads())
+                  chunk=64, max_workspace=12 << 30, e2e_chunk=2, cpu_blocks=cpu_threads())
         r5 = run_leg(args, c5, rank, world, dist, max(3, min(args.steps, 10)))
         cpu5 = cpu_leg(c5, r5) if solo and not args.no_cpu else None
         side["n1e8"] = leg_line(args, c5, r5, world, cpu5)

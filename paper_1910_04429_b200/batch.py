@@ -161,16 +161,21 @@ class HashEngine:
     def hash_seeded_host(self, x: torch.Tensor, rng_seed, first_index: int = 0,
                          out: torch.Tensor | None = None, streams: int = 3,
                          chunk: int | None = None, join_in: bool = True,
-                         join_out: bool = True) -> torch.Tensor:
+                         join_out: bool = True, seed_budget: int = 2 << 30) -> torch.Tensor:
         """run_pa's step end to end: key blocks x from (pinned) host memory, block
         first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
         derived on the GPU (only x crosses PCIe).
 
-        The seed expansion is latency-bound per XOF stream (a chain of dependent
-        Keccak-f calls), so the whole call's seeds are expanded by one launch on a
-        stream of their own, into one of two alternating buffers: the next call's
-        expansion runs beside this call's hashing.  H2D of x, hashing and D2H are
-        pipelined over `streams` slots as in hash_host (join_in / join_out as there).
+        The seed expansion is latency-bound per XOF stream: a stream's squeeze is
+        a chain of ceil(n/8)/136 dependent Keccak-f calls, whatever the number of
+        streams.  So seeds are expanded in windows of blocks, each window by one
+        launch on its own stream into its own buffer, and several windows are in
+        flight at once (up to `seed_budget` bytes of (c, d) rows): the chains of
+        all of them run concurrently, and hashing window w (chunk by chunk,
+        H2D / hash / D2H pipelined over `streams` slots as in hash_host) overlaps
+        the expansion of the windows after it.  Hand a whole key file (shard) to
+        one call: the expansion latency is then paid once per `seed_budget` of
+        blocks, not once per chunk.  join_in / join_out as in hash_host.
         """
         b = x.shape[0]
         if out is None:
@@ -178,58 +183,75 @@ class HashEngine:
         chunk = chunk or self.chunk
         nslots = max(1, streams)
         s_in, s_comp, s_out = self._pipe_streams()
-        s_seed = self._seed_stream()
         bufs = self._io_buffers(nslots, chunk)
         ev = self._slot_events(nslots)
-        sc, sd, ev_free, ev_ready = self._seed_buffers(b)
+        # windows of `win` blocks (whole hashing chunks) over `nbuf` rotating buffers:
+        # up to nbuf windows -- of this call and of the calls queued after it --
+        # expand concurrently
+        per_block = 2 * self.nbytes
+        win = max(chunk, min(-(-b // chunk) * chunk,
+                             (max(chunk, seed_budget // per_block // 4) // chunk) * chunk))
+        nbuf = max(2, min(16, seed_budget // (per_block * win)))
+        wins = self._seed_windows(nbuf, win)
         cur = torch.cuda.current_stream(self.device)
         if join_in:
             for s in (s_in, s_comp, s_out):
                 s.wait_stream(cur)
-        # the expansion reads nothing of the caller's: it only waits for its buffer
-        # (so it runs ahead, beside the previous call's hashing)
-        s_seed.wait_event(ev_free)
-        self.seed_device(rng_seed, first_index, b, sc, sd, stream=s_seed)
-        ev_ready.record(s_seed)
-        s_comp.wait_event(ev_ready)
-        for i, b0 in enumerate(range(0, b, chunk)):
-            k = i % nslots
-            dx, _, _, dout = bufs[k]
-            nb = min(chunk, b - b0)
-            s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
-            with torch.cuda.stream(s_in):
-                dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
-                ev["in"][k].record(s_in)
-            s_comp.wait_event(ev["in"][k])
-            s_comp.wait_event(ev["out"][k])      # slot k's output drained
-            self.hash_device(dx[:nb], sc[b0:b0 + nb], sd[b0:b0 + nb], dout[:nb], stream=s_comp)
-            ev["comp"][k].record(s_comp)
-            s_out.wait_event(ev["comp"][k])
-            with torch.cuda.stream(s_out):
-                out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
-                ev["out"][k].record(s_out)
-        ev_free.record(s_comp)
-        if join_out:                           # s_comp has waited for s_seed's launch
+        starts = list(range(0, b, win))
+        base = self._sw_next
+
+        def expand(w):  # window w into its rotating buffer, on that buffer's stream
+            sc, sd, ev_free, ev_ready, st = wins[(base + w) % nbuf]
+            st.wait_event(ev_free)  # the buffer's previous window is hashed
+            self.seed_device(rng_seed, first_index + starts[w], min(win, b - starts[w]), sc, sd,
+                             stream=st)
+            ev_ready.record(st)
+
+        for w in range(min(nbuf, len(starts))):
+            expand(w)
+        i = 0
+        for w, w0 in enumerate(starts):
+            sc, sd, ev_free, ev_ready, _ = wins[(base + w) % nbuf]
+            s_comp.wait_event(ev_ready)
+            for b0 in range(w0, min(b, w0 + win), chunk):
+                k = i % nslots
+                i += 1
+                dx, _, _, dout = bufs[k]
+                nb = min(chunk, b - b0)
+                s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
+                with torch.cuda.stream(s_in):
+                    dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
+                    ev["in"][k].record(s_in)
+                s_comp.wait_event(ev["in"][k])
+                s_comp.wait_event(ev["out"][k])      # slot k's output drained
+                self.hash_device(dx[:nb], sc[b0 - w0:b0 - w0 + nb], sd[b0 - w0:b0 - w0 + nb],
+                                 dout[:nb], stream=s_comp)
+                ev["comp"][k].record(s_comp)
+                s_out.wait_event(ev["comp"][k])
+                with torch.cuda.stream(s_out):
+                    out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
+                    ev["out"][k].record(s_out)
+            ev_free.record(s_comp)
+            if w + nbuf < len(starts):
+                expand(w + nbuf)
+        self._sw_next = (base + len(starts)) % nbuf
+        if join_out:  # s_comp has waited for every seed window it used
             self.join(cur)
         return out
 
-    def _seed_buffers(self, b: int):
-        """Two alternating [b, ceil(n/8)] (c, d) buffers with their free / ready events."""
-        if getattr(self, "_sb_rows", 0) < b:
-            if getattr(self, "_sb_rows", 0):
-                torch.cuda.synchronize(self.device)  # old buffers may still be in use
-            mk = lambda: torch.empty((b, self.nbytes), dtype=torch.uint8, device=self.device)  # noqa: E731
-            self._sb = [(mk(), mk(), torch.cuda.Event(), torch.cuda.Event()) for _ in range(2)]
-            self._sb_rows = b
-            self._sb_next = 0
-        c, d, free, ready = self._sb[self._sb_next]
-        self._sb_next ^= 1
-        return c[:b], d[:b], free, ready
-
-    def _seed_stream(self):
-        if not hasattr(self, "_sseed"):
-            self._sseed = torch.cuda.Stream(self.device)
-        return self._sseed
+    def _seed_windows(self, nbuf: int, win: int):
+        """nbuf rotating (c, d) window buffers [win, ceil(n/8)], each with its stream
+        and free / ready events (kept across calls, so queued calls overlap)."""
+        key = (nbuf, win)
+        if getattr(self, "_sw_key", None) != key:
+            if getattr(self, "_sw_key", None) is not None:
+                torch.cuda.synchronize(self.device)  # old windows may still be in use
+            mk = lambda: torch.empty((win, self.nbytes), dtype=torch.uint8, device=self.device)  # noqa: E731
+            self._sw = [(mk(), mk(), torch.cuda.Event(), torch.cuda.Event(),
+                         torch.cuda.Stream(self.device)) for _ in range(nbuf)]
+            self._sw_key = key
+            self._sw_next = 0
+        return self._sw
 
     def _pipe_streams(self):
         if not hasattr(self, "_pipe"):

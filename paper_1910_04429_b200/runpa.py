@@ -187,7 +187,7 @@ def shard_range(nblocks: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
-           chunk_blocks: int = 1024, seeded: SeededHasher | None = None) -> PaRunResult:
+           chunk_blocks: int | None = None, seeded: SeededHasher | None = None) -> PaRunResult:
     """Hash every complete n-bit block of cfg.in_path into r bits (bench.py:223-265).
 
     `dist` is torch.distributed (initialised) for multi-GPU runs; each rank
@@ -234,8 +234,11 @@ def run_pa(cfg: RunConfig, *, hasher: Hasher | None = None, dist=None,
     arr = np.frombuffer(data, np.uint8, count=nblocks * block_bytes).reshape(nblocks, block_bytes)
     rb = (r + 7) // 8
     parts = []
-    for b0 in range(lo, hi, chunk_blocks):
-        b1 = min(hi, b0 + chunk_blocks)
+    # one call per shard by default: the GPU seed path keeps many blocks' XOF
+    # chains in flight at once and overlaps them with the hashing
+    step = chunk_blocks or max(1, hi - lo)
+    for b0 in range(lo, hi, step):
+        b1 = min(hi, b0 + step)
         x = arr[b0:b1]
         # import_block's check: no bits beyond n (n % 8 == 0 here, so none exist)
         if seeded is not None:

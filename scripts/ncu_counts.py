@@ -16,6 +16,7 @@ METRICS = ("smsp__inst_executed.sum,smsp__thread_inst_executed.sum,"
            "smsp__issue_active.avg.pct_of_peak_sustained_active,"
            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,"
            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,"
+           "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed,"
            "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
            "smsp__cycles_elapsed.avg.per_second")
 SHAPES = {"C2": (1_000_000, 500_000, 1024), "C5": (100_000_000, 50_000_000, 64),
@@ -37,7 +38,7 @@ def run(workload):
     x, c, d = (torch.randint(0, 256, (B, nb), dtype=torch.uint8, device="cuda", generator=g)
                for _ in range(3))
     c[:, 0] |= 1
-    eng = HashEngine(n, r, max_batch=B, max_workspace=9 << 30)
+    eng = HashEngine(n, r, max_batch=B, max_workspace=12 << 30)
     assert eng.chunk == B
     out = eng.hash_device(x, c, d)
     eng.hash_device(x, c, d, out)
@@ -47,6 +48,8 @@ def run(workload):
 
 def family(name):
     base = name.split("(")[0].split("<")[0].strip()
+    if base.startswith("void "):
+        base = base[5:]
     for pre, fam in FAMILY:
         if base.startswith(pre):
             return fam
@@ -75,12 +78,13 @@ def parse(paths, out_path):
             rec = rows[key]
             fam = family(rec["name"])
             kern[fam] = {
-                "cuda_kernel": rec["name"].split("(")[0],
+                "cuda_kernel": rec["name"].split("(")[0].replace("void ", ""),
                 "inst": int(rec["smsp__inst_executed.sum"]),
                 "thread_inst": int(rec["smsp__thread_inst_executed.sum"]),
                 "issue_active": round(rec["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100, 4),
                 "pipe_alu": round(rec["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"] / 100, 4),
                 "pipe_fma": round(rec["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"] / 100, 4),
+                "pipe_fmaheavy": round(rec.get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", -100) / 100, 4),
                 "dram_bytes": int(rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]),
                 "duration_ms": round(rec["gpu__time_duration.sum"] / 1e6, 4),
                 "sm_mhz": round(rec["smsp__cycles_elapsed.avg.per_second"] / 1e6, 1),

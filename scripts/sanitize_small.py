@@ -10,8 +10,11 @@ import paper_1910_04429_b200 as pab
 
 rng = np.random.default_rng(1)
 # tiny (host path), single-CTA, four-step m=1, m=5, m=3, and a 300-block batch (seq carry)
+# + multi-tile look-back carries (k_carry_wide) over several blocks, the C2 shape
+# (cp.async-staged all-primes forward columns) and the radix-3 1e8 plan's kernels at 3e7
 for n, r, B in [(100, 33, 1), (30_000, 12_345, 2), (300_007, 150_001, 2), (2_229_060, 1_000_003, 1),
-                (2_648_360, 333_333, 1), (65_600, 32_800, 300)]:
+                (2_648_360, 333_333, 1), (65_600, 32_800, 300), (300_000, 150_011, 6),
+                (1_000_000, 500_000, 4), (30_000_000, 15_000_007, 1)]:
     nb = (n + 7) // 8
     arr = rng.integers(0, 256, size=(3, B, nb), dtype=np.uint8)
     if n % 8:
@@ -49,3 +52,16 @@ for n, r, B, order in [(1089, 100, 3, _native.ORDER_LSF), (20_001, 777, 2, _nati
 xs = rng.integers(0, 256, size=(2, 125_000), dtype=np.uint8)
 _native.hash_seeded_host(xs.tobytes(), 1_000_000, 500_000, 2, 0, first_index=3)
 print("seed paths done")
+# the drop-in's Python-int digit path and the fused multiply-add
+import random
+rr = random.Random(4)
+for n in (5_000, 300_001):
+    xv, cv, dv = rr.getrandbits(n), rr.getrandbits(n) | 1, rr.getrandbits(n)
+    got = _native.hash_ints(xv, cv, dv, n, n // 3)
+    nb = (n + 7) // 8
+    want = oracle.compress(xv.to_bytes(nb, "little"), cv.to_bytes(nb, "little"),
+                           dv.to_bytes(nb, "little"), n, n // 3)
+    assert got == int.from_bytes(want, "little")
+acc, a, b = rr.getrandbits(90_000), rr.getrandbits(50_000), rr.getrandbits(40_000)
+assert pab.fused_mul_add(acc, a, b).value == acc + a * b
+print("digit path and mul_add done")

@@ -139,3 +139,26 @@ def test_streamed_calls_without_joins():
         want = [oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r) for j in range(B)]
         assert [o[j].numpy().tobytes() for j in range(B)] == want
         assert [so[j].numpy().tobytes() for j in range(B)] == want
+
+
+@pytest.mark.parametrize("budget_blocks", [1, 4, 1000])
+def test_seed_windows_rotate_across_and_within_calls(budget_blocks):
+    # windows of seeds over rotating buffers: a budget of 1 block gives one-chunk
+    # windows over 2 buffers (rotation within a call), larger budgets several
+    # windows in flight; consecutive streamed calls continue the rotation
+    n, r, B = 50_000, 20_001, 11
+    nb = (n + 7) // 8
+    rng = np.random.default_rng(budget_blocks)
+    eng = HashEngine(n, r, max_batch=3)
+    budget = budget_blocks * 2 * nb
+    firsts = (7, 18, 7)
+    xs = [rng.integers(0, 256, size=(B, nb), dtype=np.uint8) for _ in firsts]
+    outs = [eng.hash_seeded_host(torch.from_numpy(x).pin_memory(), 5, f, join_in=i == 0,
+                                 join_out=False, seed_budget=budget)
+            for i, (x, f) in enumerate(zip(xs, firsts))]
+    eng.join()
+    torch.cuda.synchronize()
+    for x, f, o in zip(xs, firsts, outs):
+        cs, ds = host_seeds(n, 5, f, B)
+        for j in (0, 4, B - 1):
+            assert o[j].numpy().tobytes() == oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r)
