@@ -112,7 +112,7 @@ class HashEngine:
             for s in (s_in, s_comp, s_out):
                 s.wait_stream(cur)
         for i, b0 in enumerate(range(0, b, chunk)):
-            k = i % nslots
+            k = (self._slot_next + i) % nslots  # slots rotate across calls too
             dx, dc, dd, dout = bufs[k]
             nb = min(chunk, b - b0)
             s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
@@ -129,6 +129,7 @@ class HashEngine:
             with torch.cuda.stream(s_out):
                 out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
                 ev["out"][k].record(s_out)
+        self._slot_next = (self._slot_next + -(-b // chunk)) % nslots
         if join_out:
             self.join(cur)
         return out
@@ -209,7 +210,7 @@ class HashEngine:
 
         for w in range(min(nbuf, len(starts))):
             expand(w)
-        i = 0
+        i = self._slot_next  # slots rotate across calls too
         for w, w0 in enumerate(starts):
             sc, sd, ev_free, ev_ready, _ = wins[(base + w) % nbuf]
             s_comp.wait_event(ev_ready)
@@ -235,6 +236,7 @@ class HashEngine:
             if w + nbuf < len(starts):
                 expand(w + nbuf)
         self._sw_next = (base + len(starts)) % nbuf
+        self._slot_next = i % nslots
         if join_out:  # s_comp has waited for every seed window it used
             self.join(cur)
         return out
@@ -260,6 +262,7 @@ class HashEngine:
 
     def _slot_events(self, k: int):
         if getattr(self, "_ev_k", None) != k:
+            self._slot_next = 0
             if getattr(self, "_ev_k", None) is not None:
                 self.join()  # earlier calls' copies / hashing may still wait on the old events
             mk = lambda: [torch.cuda.Event() for _ in range(k)]  # noqa: E731

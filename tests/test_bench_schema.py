@@ -10,7 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def latest(pattern):
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r1", pattern)))  # r1a < r1b < ...
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r2", pattern)))  # r2a < r2b < ...
+    if not files:
+        files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r1", pattern)))
     if not files:
         pytest.skip(f"no {pattern} evidence")
     with open(files[-1]) as f:
@@ -18,7 +20,8 @@ def latest(pattern):
 
 
 def test_ours_line_keys():
-    d = latest("bench_r1?.json")
+    d = latest("bench_r2?.json") if glob.glob(os.path.join(ROOT, "profiles", "r2", "bench_r2?.json")) \
+        else latest("bench_r1?.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
               "gpu_launches", "roofline", "cpu_baseline", "clocks"):
@@ -29,8 +32,16 @@ def test_ours_line_keys():
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor") and r["peak"] > 0
+    assert r["bound"] in ("hbm", "tensor", "int") and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    if r["bound"] == "int":  # executed-instruction issue fraction agrees with ncu issue-active
+        assert abs(r["frac"] - r["ncu"]["issue_active"]) <= 0.05
+        assert r["traffic"] > 0
+    if "n1e8" in d:  # BASELINE configs[4] (C5) leg with its own e2e / cpu_baseline / roofline
+        c5 = d["n1e8"]
+        assert c5["config"]["workload"] == "C5" and c5["config"]["blocks_per_rank"] == 64
+        assert c5["e2e"]["value"] > 0 and c5["cpu_baseline"]["bit_exact_vs_gpu"]
+        assert c5["roofline"]["traffic"] and [x["ratio"] for x in c5["ratio_sweep"]] == [0.1, 0.9]
     c = d["cpu_baseline"]
     assert c["kind"] in ("port", "reference") and c["cores"] >= 1 and c["bit_exact_vs_gpu"]
     ck = d["clocks"]
@@ -38,7 +49,8 @@ def test_ours_line_keys():
 
 
 def test_reference_line_keys():
-    d = latest("bench_ref_r1?.json")
+    d = latest("bench_ref_r2?.json") if glob.glob(os.path.join(ROOT, "profiles", "r2", "bench_ref_r2?.json")) \
+        else latest("bench_ref_r1?.json")
     assert d["impl"] == "reference"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["value"] == d["value"]
