@@ -37,7 +37,7 @@ def test_ours_line_keys():
     if r["bound"] == "int":  # executed-instruction issue fraction agrees with ncu issue-active
         assert abs(r["frac"] - r["ncu"]["issue_active"]) <= 0.05
         assert r["traffic"] > 0
-    if "n1e8" in d:  # BASELINE configs[4] (C5) leg with its own e2e / cpu_baseline / roofline
+    if "config" in d.get("n1e8", {}):  # BASELINE configs[4] (C5) leg with its own e2e / cpu_baseline / roofline
         c5 = d["n1e8"]
         assert c5["config"]["workload"] == "C5" and c5["config"]["blocks_per_rank"] == 64
         assert c5["e2e"]["value"] > 0 and c5["cpu_baseline"]["bit_exact_vs_gpu"]
