@@ -162,18 +162,17 @@ __device__ __forceinline__ void stage_operand(const OpView& ov, uint2* stage, in
                                               int lgC, int c0) {
   const int lct = LCT >= 0 ? LCT : lct_in;
   const int CT = 1 << lct;
-  int e0 = 0;  // first staged element that needs the checked path
-  if (ov.cw == 2 && ov.a8) {
-    // rows < rows - 1 hold only valid, unmasked coefficients (rows = ceil(kc / C),
-    // so (rows - 1) C <= kc - 1); the last row too unless the tile reaches kc - 1
-    const bool last_full = ((rows - 1) << lgC) + c0 + CT - 1 < ov.kc - 1;
-    e0 = (last_full ? rows : rows - 1) << lct;
-    for (int e = threadIdx.x; e < e0; e += blockDim.x) {
+  if (ov.cw == 2 && ov.a8 && ((rows - 1) << lgC) + c0 + CT - 1 < ov.kc - 1) {
+    // every staged coefficient valid and unmasked (all but the operand's last tiles)
+    for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
       const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
       cp_async8(stage + e, ov.src + 2 * gi);
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    return;
   }
-  for (int e = e0 + threadIdx.x; e < (rows << lct); e += blockDim.x) {
+  for (int e = threadIdx.x; e < (rows << lct); e += blockDim.x) {
     const int gi = ((e >> lct) << lgC) + c0 + (e & (CT - 1));
     if (gi < ov.kc - 1) {
       if (ov.cw == 2) {
