@@ -136,9 +136,6 @@ def kernel_model(n: int, r: int, blocks: int) -> dict:
     m["k_unpack"] = dict(bytes=blocks * (4 * mw + rb), ops=0)
     m["k_carry"] = dict(bytes=blocks * (P * 4 * Kc + 4 * K + 4 * mw),
                         ops=blocks * (Kc * crt + K * 25))
-    if mr == 1 and L == 1 << 15 and g["cw"] == 2:  # fused two-CTA-cluster path (fused15.cu)
-        m["k_conv_fused"] = dict(bytes=blocks * (2 * 4 * K + P * 4 * Kc),
-                                 ops=blocks * P * (3 * bf(lgR + lgC) * 7 + L * 6 + 2 * Kc * 9))
     if lgR == 0:
         m["k_row_single"] = dict(bytes=blocks * (2 * 4 * K + P * 4 * Kc),
                                  ops=blocks * P * (3 * bf(lgC) * 7 + L * 6 + 2 * red_in))

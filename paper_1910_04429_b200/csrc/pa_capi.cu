@@ -152,8 +152,7 @@ struct Plan {
   uint2* trad = nullptr;
   int tstride = 0;
   uint2* tw4 = nullptr;
-  uint2* stwL = nullptr;
-  u32 scale[kNumPrimes], scale_sh[kNumPrimes], scale2[kNumPrimes], scale2_sh[kNumPrimes];
+  u32 scale[kNumPrimes], scale_sh[kNumPrimes];
 };
 
 struct HostCtx {  // cached buffers for the host-pointer entry points
@@ -278,7 +277,7 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
   const int slo0 = pass_plan(geo.lgC).slo[0];
   for (int i = 0; i < kNumPrimes; ++i) {
     const u32 p = kPrimes[i];
-    pl.scale[i] = pl.scale_sh[i] = pl.scale2[i] = pl.scale2_sh[i] = 0;
+    pl.scale[i] = pl.scale_sh[i] = 0;
     if ((p - 1) % L != 0) continue;  // a cw = 1 length beyond this prime's 2-adicity
     const u64 r32 = ((u64)1 << 32) % p;
     // L^-1 * 2^32: undoes the length and the Montgomery factor of the pointwise
@@ -289,8 +288,6 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
     const u64 sc = linv * r32 % p;
     pl.scale[i] = (u32)sc;
     pl.scale_sh[i] = shoup_of(pl.scale[i], p);
-    pl.scale2[i] = (u32)(sc * r32 % p);
-    pl.scale2_sh[i] = shoup_of(pl.scale2[i], p);
     for (int dir = 0; dir < 2; ++dir) {
       const size_t pd = (size_t)i * 2 + dir;
       const u32 wL = root_of(i, L, dir);
@@ -351,26 +348,6 @@ int get_plan(DevState* ds, const Geo& geo, const Plan** out) {
     for (auto& w : workers) w.join();
     if ((rc = upload((void**)&pl.tw4, t4.data(), t4.size() * sizeof(uint2)))) return rc;
   }
-  // full-length stage twiddles for the fused two-CTA convolution (fused15.cu, L = 2^15)
-  if (geo.m == 1 && L == ((u64)1 << 15)) {
-    std::vector<uint2> st((size_t)kNumPrimes * 2 * L, make_uint2(0, 0));
-    for (int i = 0; i < kNumPrimes; ++i) {
-      const u32 p = kPrimes[i];
-      if ((p - 1) % L != 0) continue;
-      for (int dir = 0; dir < 2; ++dir) {
-        uint2* tw = &st[((size_t)i * 2 + dir) * L];
-        for (u64 h = 1; h < L; h <<= 1) {  // tw[h + e] = w_2h^e, e < h
-          const u32 w = root_of(i, 2 * h, dir);
-          u64 x = 1;
-          for (u64 e = 0; e < h; ++e) {
-            tw[h + e] = make_uint2((u32)x, shoup_of((u32)x, p));
-            x = x * w % p;
-          }
-        }
-      }
-    }
-    if ((rc = upload((void**)&pl.stwL, st.data(), st.size() * sizeof(uint2)))) return rc;
-  }
   auto res = ds->plans.emplace(key, pl);
   *out = &res.first->second;
   return PAB_OK;
@@ -386,12 +363,9 @@ PlanTables tables_of(const DevState* ds, const Plan* pl) {
   t.trad = pl->trad;
   t.tstride = pl->tstride;
   t.tw4 = pl->tw4;
-  t.stwL = pl->stwL;
   for (int i = 0; i < kNumPrimes; ++i) {
     t.scale[i] = pl->scale[i];
     t.scale_sh[i] = pl->scale_sh[i];
-    t.scale2[i] = pl->scale2[i];
-    t.scale2_sh[i] = pl->scale2_sh[i];
   }
   return t;
 }

@@ -1273,15 +1273,6 @@ static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
 
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
-  static const bool fused_off = [] {  // development switch: PAB_FUSED=0 keeps the four-step path
-    const char* e = getenv("PAB_FUSED");
-    return e && e[0] == '0';
-  }();
-  if (!fused_off && fused15_applies(job, tab)) {
-    prof::Scope ps_("k_conv_fused", st);
-    launch_fused15(job, tab, st);
-    return;
-  }
   if (job.m == 1 && job.lgR == 0) {
     const size_t sm = (size_t)sm_len(job.lgC) * 2 * 4;
     prof::Scope ps_("k_row_single", st);
@@ -1403,7 +1394,6 @@ void launch_carry(const ConvJob& job, cudaStream_t st) {
 
 // Opt every dynamic-smem kernel into > 48 KB once per device.
 void set_kernel_attrs() {
-  set_fused15_attrs();
   for (int lg = 1; lg <= 12; ++lg) {
     for (int s = 0; s < 2; ++s) {
       ConvKernel k = row_kernel(lg, s != 0);

@@ -21,10 +21,6 @@ struct PlanTables {
                        // Shoup pairs; only for small L (L2-resident), else null
   u32 scale[kNumPrimes];     // L^-1 * 2^32 mod p: undoes the length and the Montgomery
   u32 scale_sh[kNumPrimes];  // factor of the pointwise product (Shoup companions)
-  u32 scale2[kNumPrimes];    // scale * 2^32 mod p (the high word of a 64-bit coefficient)
-  u32 scale2_sh[kNumPrimes];
-  const uint2* stwL;   // [5][2][L] stage twiddles tw[h + e] = w_2h^e for h < L (fused
-                       // L = 2^15 path only), else null
 };
 
 // One convolution-product job over a batch of independent blocks:
@@ -127,10 +123,6 @@ void launch_seed_expand(const SeedMaster& master, int mlen, unsigned long long f
 void seed_expand_raw(const SeedMaster& master, int mlen, unsigned long long first, int batch,
                      long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
                      long long stride, cudaStream_t st);
-// fused two-CTA-cluster convolution for L = 2^15 (fused15.cu)
-bool fused15_applies(const ConvJob& job, const PlanTables& tab);
-void launch_fused15(const ConvJob& job, const PlanTables& tab, cudaStream_t st);
-void set_fused15_attrs();
 // a kernel set exists for this geometry (L = m * 2^(lgR + lgC))
 bool conv_supported(int m, int lgR, int lgC);
 

@@ -24,7 +24,7 @@ SHAPES = {"C2": (1_000_000, 500_000, 1024), "C5": (100_000_000, 50_000_000, 64),
 # CUDA kernel name -> the launcher's profile name (bench.py's kernel table)
 FAMILY = (("k_col_fwd", "k_col_fwd"), ("k_colm_fwd", "k_col_fwd"), ("k_col_inv", "k_col_inv"),
           ("k_colm_inv", "k_col_inv"), ("k_carry", "k_carry"), ("k_row", "k_row"),
-          ("k_pack", "k_pack"), ("k_unpack", "k_unpack"), ("k_conv_fused", "k_conv_fused"))
+          ("k_pack", "k_pack"), ("k_unpack", "k_unpack"))
 
 
 def run(workload):
