@@ -13,8 +13,13 @@ scaling (blocks shard by index, no collective on the data path).
 127.0.0.1); under torchrun WORLD_SIZE must equal N.
 
 `value`  : device-resident Mbps (inputs already in HBM), max-over-ranks time.
-`e2e`    : same metric through the public batched API from pinned host memory,
-           H2D of x, c, d and D2H of the keys inside the timed region.
+`e2e`    : same metric and the same blocks through the public batched API from
+           pinned host memory, every copy inside the timed region: the key blocks x
+           go H2D, each block's (c, d) -- BASELINE's per-block seeds, derived as the
+           reference bench protocol does (gen_seed(n, derive_block_seed(s, n))) -- is
+           expanded on the GPU, the keys come back D2H; bit-identical to `value`'s
+           keys.  `e2e.xcd` ships x, c and d instead (the only e2e at n=1e8, where one
+           seed stream is a ~0.3 s Keccak chain).
 `e2e_run_pa`: run_pa's scope (n <= 1e7): only the key blocks x cross PCIe; each
            block's (c, d) is expanded on the GPU (SHAKE-256) beside the hashing.
 `roofline`: the dominant kernel against the integer-issue roofline (148 SMs x
@@ -22,7 +27,7 @@ scaling (blocks shard by index, no collective on the data path).
            instructions from the committed ncu counts of the same batch; HBM beside.
 `n1e8`   : BASELINE configs[4] (C5): 64 blocks/rank at n=1e8, m/n 0.5 timed with its
            own e2e, cpu_baseline and roofline; m/n 0.1 and 0.9 as `ratio_sweep`.
-`c4`     : BASELINE configs[3]: one n=1e8 block, device latency.
+`c1`, `c4`: BASELINE configs[0] / [3]: one n=1e6 / n=1e8 block, device latency.
 `--impl reference`: the reference's CPU algorithm (the C port under oracle/,
            all host threads, rank 0 only) on the same 1024 C2 blocks per step.
 `--dry-run`: CPU only (gloo): the launcher, rank plumbing and JSON line, no kernels.
@@ -362,7 +367,6 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
     eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
-    clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
     assert torch.equal(hout, first_out), "e2e keys differ from device-resident keys"
     # the PCIe bound of that leg: the same pinned H2D + D2H bytes, copies only
@@ -385,14 +389,46 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
     c1.record(st)
     torch.cuda.synchronize()
     copy_ms = max_over_ranks(c0.elapsed_time(c1) / reps, dist)
-    e2e = {"value": round(bits_step / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
-           "h2d_bytes_per_step": 3 * per_rank * eng.nbytes,
-           "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(e2e_ms, 4),
-           "copy_only_ms_per_step": round(copy_ms, 4),
-           "h2d_gbps": round(3 * per_rank * eng.nbytes / (e2e_ms * 1e-3) / 1e9, 1),
-           "frac_of_copy_bound": round(copy_ms / e2e_ms, 4),
-           "scope": "HashEngine.hash_host: pinned x, c, d -> GPU, keys -> pinned host, "
-                    "consecutive steps streamed"}
+    e2e_xcd = {"value": round(bits_step / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
+               "h2d_bytes_per_step": 3 * per_rank * eng.nbytes,
+               "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(e2e_ms, 4),
+               "copy_only_ms_per_step": round(copy_ms, 4),
+               "h2d_gbps": round(3 * per_rank * eng.nbytes / (e2e_ms * 1e-3) / 1e9, 1),
+               "frac_of_copy_bound": round(copy_ms / e2e_ms, 4),
+               "scope": "HashEngine.hash_host: pinned x, c, d -> GPU, keys -> pinned host, "
+                        "consecutive steps streamed"}
+    # headline e2e (n <= 1e7): the same blocks, only the key blocks x cross PCIe; each
+    # block's (c, d) = gen_seed(n, derive_block_seed(s, n)) -- BASELINE's per-block
+    # seeds, the reference bench protocol -- is expanded on the GPU in the timed region.
+    # At 1e8 one seed stream is a 92K-permutation chain (~0.3 s), so there the e2e is
+    # the (x, c, d) copy path.
+    e2e = e2e_xcd
+    if n <= 10_000_000 and seeds == list(range(seeds[0], seeds[0] + per_rank)):
+        sout = torch.empty(hout.shape, dtype=torch.uint8, pin_memory=True)
+        for _ in range(max(1, args.warmup)):
+            eng.hash_seeded_host(px, None, seeds[0], sout, protocol="bench")
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for i in range(steps):
+            eng.hash_seeded_host(px, None, seeds[0], sout, join_in=i == 0, join_out=False,
+                                 protocol="bench")
+        eng.join(st)
+        e1.record(st)
+        torch.cuda.synchronize()
+        s_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
+        assert torch.equal(sout, first_out), "seeded e2e keys differ from device-resident keys"
+        e2e = {"value": round(bits_step / (s_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
+               "h2d_bytes_per_step": per_rank * eng.nbytes,
+               "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(s_ms, 4),
+               "scope": "HashEngine.hash_seeded_host(protocol='bench'): pinned x -> GPU, each "
+                        "block's (c, d) = gen_seed(n, derive_block_seed(s, n)) expanded on the "
+                        "GPU (SHAKE-256), keys -> pinned host, consecutive steps streamed; keys "
+                        "bit-identical to the device-resident leg",
+               "xcd": e2e_xcd}
+    clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
 
     e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) \
         if n <= 10_000_000 else None
@@ -625,14 +661,15 @@ def cpu_leg(cfg, res) -> dict:
     return cpu
 
 
-def c4_leg(args, dist) -> dict:
-    """BASELINE configs[3]: one n=1e8 block (seed 7), r=5e7 -- device latency of the
-    largest single product, per-kernel times and the drop-in compress call."""
+def single_leg(args, dist, name: str = "C4") -> dict:
+    """A single-block config: BASELINE configs[0] (C1: n=1e6, seed 0) or configs[3]
+    (C4: n=1e8, seed 7) -- device latency of one block's hash, per-kernel times and
+    the drop-in compress call on the same block."""
     import torch
     from paper_1910_04429_b200 import workloads
     from paper_1910_04429_b200.batch import HashEngine
 
-    cfg = workloads.CONFIGS["C4"]
+    cfg = workloads.CONFIGS[name]
     n, r = cfg["n"], cfg["ms"][0]
     xs, cs, ds = workloads.batch_inputs(n, cfg["seeds"])
     dx, dc, dd = (torch.from_numpy(a).cuda() for a in (xs, cs, ds))
@@ -641,12 +678,13 @@ def c4_leg(args, dist) -> dict:
     steps = max(3, min(args.steps, 20))
     ms, prof = time_device(eng, dx, dc, dd, dout, steps, 3, dist)
     ms = max_over_ranks(ms / steps, dist)
-    roof, kernels = roofline_obj(prof, n, r, 1, "C4", None)
-    out = {"workload": "C4: 1 block, n=1e8, r=5e7, seed 7", "ms_per_block": round(ms, 4),
+    roof, kernels = roofline_obj(prof, n, r, 1, name, None)
+    out = {"workload": f"{name}: 1 block, n={n}, r={r}, seed {cfg['seeds'][0]}",
+           "ms_per_block": round(ms, 4),
            "value": round(n / (ms * 1e-3) / 1e6, 1), "unit": "Mbps", "steps": steps,
            "kernels": kernels, "roofline": roof}
     if not args.no_extra and (not dist or dist.get_rank() == 0):
-        out["dropin"] = dropin_timing(n, r, calls=3)
+        out["dropin"] = dropin_timing(n, r, calls=3 if n > 10_000_000 else 10)
     return out
 
 
@@ -773,7 +811,8 @@ def main():
         side["n1e8"] = leg_line(args, c5, r5, world, cpu5)
         del r5
         torch.cuda.empty_cache()
-        side["c4"] = c4_leg(args, dist)
+        side["c4"] = single_leg(args, dist, "C4")
+        side["c1"] = single_leg(args, dist, "C1")
 
     if rank == 0:
         out = {"metric": METRIC, "value": line.pop("value"), "unit": "Mbps", "n_gpus": world,

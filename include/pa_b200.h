@@ -158,6 +158,16 @@ int pab_seed_expand(const uint8_t* master, uint64_t master_len, uint64_t first_i
                     uint64_t stride, void* stream);
 
 /*
+ * Seed expansion of the reference's benchmark protocol (pkg/src/modpa/bench.py:156,
+ * run_bench's inputs; BASELINE configs' per-block seeds): block j gets
+ *   gen_seed(n, derive_block_seed(s, index)),   s = first_seed + j,
+ * i.e. the integer s itself is the seed material and the label index is fixed
+ * (the reference passes index = n).  Outputs and layout as pab_seed_expand.
+ */
+int pab_seed_expand_bench(uint64_t first_seed, uint32_t batch, uint64_t index, uint64_t n_bits,
+                          int byte_order, uint8_t* c, uint8_t* d, uint64_t stride, void* stream);
+
+/*
  * Host-buffer run_pa step on `device` (pkg/src/modpa/bench.py:256-262 for a
  * contiguous run of blocks): x = batch*ceil(n/8) host bytes (blocks first_index
  * .. first_index+batch-1 of the key file), seeds derived on the device by

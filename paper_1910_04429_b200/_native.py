@@ -53,6 +53,9 @@ SIGNATURES = {
     "pab_seed_expand": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                        ctypes.c_uint64, ctypes.c_int, _u8p, _u8p,
                                        ctypes.c_uint64, _u8p]),
+    "pab_seed_expand_bench": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_int, _u8p, _u8p,
+                                             ctypes.c_uint64, _u8p]),
     "pab_hash_seeded_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_uint64,
                                             ctypes.c_uint64, _u8p, ctypes.c_int]),

@@ -141,10 +141,17 @@ class HashEngine:
             cur.wait_stream(s)
 
     def seed_device(self, rng_seed, first_index: int, batch: int, c: torch.Tensor,
-                    d: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
-        """(c, d) of blocks first_index .. first_index+batch-1 as run_pa derives them,
-        gen_seed(n, derive_block_seed(rng_seed, i)) (pkg/src/modpa/pa.py:138-172),
-        SHAKE-256 on the device into rows of c and d (asynchronous on `stream`)."""
+                    d: torch.Tensor, stream: torch.cuda.Stream | None = None,
+                    protocol: str = "run_pa") -> None:
+        """(c, d) of blocks first_index .. first_index+batch-1, SHAKE-256 on the device
+        into rows of c and d (asynchronous on `stream`), derived as
+          protocol "run_pa": gen_seed(n, derive_block_seed(rng_seed, i))
+                             (pkg/src/modpa/bench.py:258, pa.py:138-172);
+          protocol "bench":  gen_seed(n, derive_block_seed(i, n)) -- the reference's
+                             benchmark inputs (bench.py:156), i = the block seed,
+                             rng_seed unused (BASELINE configs' per-block seeds)."""
+        if protocol not in ("run_pa", "bench"):
+            raise ValueError(f"unknown seed protocol {protocol!r}")
         for t in (c, d):
             if t.device != self.device or t.dtype != torch.uint8 or t.dim() != 2:
                 raise ValueError("c, d must be 2-D uint8 tensors on the engine's device")
@@ -152,9 +159,14 @@ class HashEngine:
                 raise ValueError("c, d must be [>= batch, >= ceil(n/8)] with unit byte stride")
         if c.stride(0) != d.stride(0):
             raise ValueError("c and d must share one row stride")
-        m = _native.seed_material(rng_seed)
         st = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
+            if protocol == "bench":
+                _native.check(self.lib.pab_seed_expand_bench(
+                    first_index, batch, self.n, self.n, self.order, _ptr(c), _ptr(d), c.stride(0),
+                    ctypes.c_void_p(st.cuda_stream)))
+                return
+            m = _native.seed_material(rng_seed)
             _native.check(self.lib.pab_seed_expand(
                 m, len(m), first_index, batch, self.n, self.order, _ptr(c), _ptr(d), c.stride(0),
                 ctypes.c_void_p(st.cuda_stream)))
@@ -162,10 +174,12 @@ class HashEngine:
     def hash_seeded_host(self, x: torch.Tensor, rng_seed, first_index: int = 0,
                          out: torch.Tensor | None = None, streams: int = 3,
                          chunk: int | None = None, join_in: bool = True,
-                         join_out: bool = True, seed_budget: int = 2 << 30) -> torch.Tensor:
+                         join_out: bool = True, seed_budget: int = 2 << 30,
+                         protocol: str = "run_pa") -> torch.Tensor:
         """run_pa's step end to end: key blocks x from (pinned) host memory, block
         first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
-        derived on the GPU (only x crosses PCIe).
+        derived on the GPU (only x crosses PCIe); protocol "bench" derives the
+        reference benchmark's seeds instead (see seed_device).
 
         The seed expansion is latency-bound per XOF stream: a stream's squeeze is
         a chain of ceil(n/8)/136 dependent Keccak-f calls, whatever the number of
@@ -205,7 +219,7 @@ class HashEngine:
             sc, sd, ev_free, ev_ready, st = wins[(base + w) % nbuf]
             st.wait_event(ev_free)  # the buffer's previous window is hashed
             self.seed_device(rng_seed, first_index + starts[w], min(win, b - starts[w]), sc, sd,
-                             stream=st)
+                             stream=st, protocol=protocol)
             ev_ready.record(st)
 
         for w in range(min(nbuf, len(starts))):

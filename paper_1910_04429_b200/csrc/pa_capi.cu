@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <climits>
 #include <cstring>
 #include <atomic>
 #include <map>
@@ -828,6 +829,28 @@ int pab_seed_expand(const uint8_t* master, uint64_t master_len, uint64_t first_i
   launch_seed_expand(sm, (int)master_len, (unsigned long long)first_index, (int)batch,
                      (long long)n_bits, msf, word_io, c, d, (long long)stride,
                      (cudaStream_t)stream);
+  CK(cudaGetLastError(), "kernel launch");
+  return PAB_OK;
+}
+
+int pab_seed_expand_bench(uint64_t first_seed, uint32_t batch, uint64_t index, uint64_t n_bits,
+                          int byte_order, uint8_t* c, uint8_t* d, uint64_t stride, void* stream) {
+  if (n_bits < 1) return fail(PAB_EINVAL, "alpha must be >= 1, got 0");
+  if (n_bits > ((u64)1 << 40)) return fail(PAB_ERANGE, "block size beyond the seed expander");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  if (batch == 0) return PAB_OK;
+  if (!c || !d) return fail(PAB_EINVAL, "null pointer argument");
+  const u64 nbytes = ceil_div(n_bits, 8);
+  if (stride < nbytes) return fail(PAB_EINVAL, "stride smaller than the block byte length");
+  if (first_seed > ~0ull - batch) return fail(PAB_EINVAL, "block seed overflows 64 bits");
+  if (index > (u64)LLONG_MAX) return fail(PAB_EINVAL, "label index beyond 2^63");
+  SeedMaster sm;
+  std::memset(&sm, 0, sizeof(sm));
+  const int msf = byte_order == PAB_ORDER_MSF;
+  const int word_io = !msf && stride % 8 == 0 && aligned(c, 8) && aligned(d, 8);
+  launch_seed_expand(sm, 0, (unsigned long long)first_seed, (int)batch, (long long)n_bits, msf,
+                     word_io, c, d, (long long)stride, (cudaStream_t)stream, (long long)index);
   CK(cudaGetLastError(), "kernel launch");
   return PAB_OK;
 }

@@ -100,9 +100,10 @@ int profile_collect(const char** names, int* counts, double* ms, int cap) {
 
 void launch_seed_expand(const SeedMaster& master, int mlen, unsigned long long first, int batch,
                         long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
-                        long long stride, cudaStream_t st) {
+                        long long stride, cudaStream_t st, long long fixed_index) {
   prof::Scope ps_("k_seed_expand", st);
-  seed_expand_raw(master, mlen, first, batch, n_bits, msf, word_io, c, d, stride, st);
+  seed_expand_raw(master, mlen, first, batch, n_bits, msf, word_io, c, d, stride, st,
+                  fixed_index);
 }
 
 // ---------------------------------------------------------------------------

@@ -117,12 +117,14 @@ constexpr int kMaxSeedMaster = 1024;  // master seed material bytes (kernel para
 struct SeedMaster {
   uint8_t b[kMaxSeedMaster];
 };
+// fixed_index >= 0: the bench protocol -- block j's material is the integer
+// first + j and the derive_block_seed label index is fixed_index (master unused)
 void launch_seed_expand(const SeedMaster& master, int mlen, unsigned long long first, int batch,
                         long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
-                        long long stride, cudaStream_t st);
+                        long long stride, cudaStream_t st, long long fixed_index = -1);
 void seed_expand_raw(const SeedMaster& master, int mlen, unsigned long long first, int batch,
                      long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
-                     long long stride, cudaStream_t st);
+                     long long stride, cudaStream_t st, long long fixed_index);
 // a kernel set exists for this geometry (L = m * 2^(lgR + lgC))
 bool conv_supported(int m, int lgR, int lgC);
 

@@ -209,26 +209,36 @@ __device__ __forceinline__ int dec_len(unsigned long long v) {
 
 // Lane pair s = t / 2 of the grid owns XOF stream s: block j = s / 2 (index
 // first + j), stream s % 2 (0: c, 1: d); lane parity = which half it holds.
+// fixed_index < 0 (run_pa, pkg/src/modpa/bench.py:258): block j's seed is
+//   gen_seed(n, derive_block_seed(master, first + j));
+// fixed_index >= 0 (the reference's bench protocol, bench.py:156): block j's
+// seed material is the integer s = first + j itself and the label index is fixed,
+//   gen_seed(n, derive_block_seed(s, fixed_index))   (fixed_index = n there).
 __global__ void __launch_bounds__(64) k_seed_expand(const SeedMaster master, int mlen,
                                                      unsigned long long first, int batch,
                                                      long long n_bits, int msf, int word_io,
                                                      uint8_t* __restrict__ c,
-                                                     uint8_t* __restrict__ d, long long stride) {
+                                                     uint8_t* __restrict__ d, long long stride,
+                                                     long long fixed_index) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t par = t & 1;
   const int s_raw = t >> 1;
   const bool active = s_raw < 2 * batch;  // idle pairs still shuffle with the warp
   const int s = active ? s_raw : 2 * batch - 1;
   const int j = s >> 1, which = s & 1;
-  const unsigned long long idx = first + (unsigned long long)j;
+  const unsigned long long blk = first + (unsigned long long)j;
+  const bool bench = fixed_index >= 0;
+  // derive_block_seed(material, idx): label b"block-%d" % idx
+  const unsigned long long idx = bench ? (unsigned long long)fixed_index : blk;
+  // an int seed s is s.to_bytes(max(1, ceil(bitlen / 8)), "little") (pa.py:141-146)
+  const int ml = bench ? (blk ? (64 - __clzll((long long)blk) + 7) / 8 : 1) : mlen;
   uint32_t A[25];
-  // derive_block_seed(master, idx): label b"block-%d" % idx
   const int dl = dec_len(idx);
   const int llen = 6 + dl;  // "block-" + digits
   {
 #pragma unroll
     for (int i = 0; i < 25; ++i) A[i] = 0;
-    const int len = 2 + llen + 4 + mlen;
+    const int len = 2 + llen + 4 + ml;
     absorb(A, par, len, [&](int k) -> uint8_t {
       if (k < 2) return (uint8_t)(llen >> (8 * k));
       k -= 2;
@@ -239,8 +249,8 @@ __global__ void __launch_bounds__(64) k_seed_expand(const SeedMaster master, int
         return (uint8_t)('0' + v % 10);
       }
       k -= llen;
-      if (k < 4) return (uint8_t)((unsigned)mlen >> (8 * k));
-      return master.b[k - 4];
+      if (k < 4) return (uint8_t)((unsigned)ml >> (8 * k));
+      return bench ? (uint8_t)(blk >> (8 * (k - 4))) : master.b[k - 4];
     });
   }
   uint64_t S[4];  // 32-byte block seed = first four lanes
@@ -313,12 +323,12 @@ __global__ void __launch_bounds__(64) k_seed_expand(const SeedMaster master, int
 // (pa_kernels.cu's launch_seed_expand wraps this with the profiling scope)
 void seed_expand_raw(const SeedMaster& master, int mlen, unsigned long long first, int batch,
                      long long n_bits, int msf, int word_io, uint8_t* c, uint8_t* d,
-                     long long stride, cudaStream_t st) {
+                     long long stride, cudaStream_t st, long long fixed_index) {
   const int threads = 4 * batch;  // a lane pair per XOF stream, two streams per block
   const int per = 64;  // two warps per CTA: the few streams spread over the SMs
   const dim3 grid((threads + per - 1) / per);
   k_seed_expand<<<grid, per, 0, st>>>(master, mlen, first, batch, n_bits, msf, word_io, c, d,
-                                      stride);
+                                      stride, fixed_index);
 }
 
 }  // namespace pab

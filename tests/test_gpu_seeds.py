@@ -162,3 +162,30 @@ def test_seed_windows_rotate_across_and_within_calls(budget_blocks):
         cs, ds = host_seeds(n, 5, f, B)
         for j in (0, 4, B - 1):
             assert o[j].numpy().tobytes() == oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r)
+
+
+def test_bench_protocol_seeds_match_the_reference_workload():
+    # pab_seed_expand_bench: block seed s -> gen_seed(n, derive_block_seed(s, n)), the
+    # reference benchmark's (c, d) (pkg/src/modpa/bench.py:156; workloads.block_inputs)
+    from paper_1910_04429_b200 import workloads
+
+    for n, first, B in ((1_000_000, 0, 3), (4_099, 255, 4), (130_001, 65_534, 3)):
+        nb = (n + 7) // 8
+        eng = HashEngine(n, n // 2, max_batch=B)
+        c = torch.empty((B, nb + 8), dtype=torch.uint8, device="cuda")
+        d = torch.empty_like(c)
+        eng.seed_device(None, first, B, c, d, protocol="bench")
+        torch.cuda.synchronize()
+        for j in range(B):
+            _, cw, dw = workloads.block_inputs(n, first + j)
+            assert c[j, :nb].cpu().numpy().tobytes() == cw, (n, first + j)
+            assert d[j, :nb].cpu().numpy().tobytes() == dw, (n, first + j)
+    # the seeded engine path on the benchmark protocol equals hashing host (x, c, d)
+    n, r, B = 200_000, 99_999, 5
+    xs, cs, ds = workloads.batch_inputs(n, range(10, 10 + B))
+    eng = HashEngine(n, r, max_batch=2)
+    got = eng.hash_seeded_host(torch.from_numpy(xs).pin_memory(), None, 10, protocol="bench")
+    torch.cuda.synchronize()
+    for j in range(B):
+        assert got[j].numpy().tobytes() == oracle.compress(xs[j].tobytes(), cs[j].tobytes(),
+                                                           ds[j].tobytes(), n, r)

@@ -146,3 +146,20 @@ def test_run_pa_gpu_host_seeds_matches_reference_files(tmp_path):
         cfg, out = _cfg(case, tmp_path, "h" + str(i))
         run_pa(cfg, hasher=gpu_hasher(), chunk_blocks=3)
         assert out.read_bytes().hex() == case["out"], case["n"]
+
+
+@pytest.mark.gpu
+def test_run_pa_gpu_long_seed_material(tmp_path):
+    # seed material beyond the device expander's 1 KiB (an rng_seed >= 2^8192):
+    # run_pa derives the seeds on the host instead and still hashes on the GPU
+    big = (1 << 9000) + 12345
+    rng = np.random.default_rng(9)
+    key = tmp_path / "k.bin"
+    key.write_bytes(rng.integers(0, 256, size=3 * 512, dtype=np.uint8).tobytes())
+    outs = []
+    for tag, kw in (("gpu", {}), ("oracle", {"hasher": oracle_hasher})):
+        out = tmp_path / f"{tag}.bin"
+        run_pa(RunConfig(sizes=(4096,), ratio=0.5, rng_seed=big, in_path=str(key),
+                         out_path=str(out)), **kw)
+        outs.append(out.read_bytes())
+    assert outs[0] == outs[1] and len(outs[0]) == 3 * 256
