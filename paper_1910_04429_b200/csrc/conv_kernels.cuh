@@ -1121,9 +1121,12 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
   for (int i = threadIdx.x; i < job.np * NTW; i += blockDim.x)
     s_tw[i] = __ldg(tab.stw + ((i / NTW) * 2) * kTwN + (i % NTW));
   stage_operand<lct>(ov, stage, rows, lct, LGC, tile << lct);  // (its barrier covers s_tw too)
+  // small launches (few blocks) spread the primes over grid.y, one per CTA
+  const int q0 = gridDim.y > 1 ? job.p0 + (int)blockIdx.y : job.p0;
+  const int qn = gridDim.y > 1 ? 1 : job.pn;
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
-    if (P >= job.p0 && P < job.p0 + job.pn) {
+    if (P >= q0 && P < q0 + qn) {
       col_fwd_body<P, LGR, LGC, true, lct>(job, tab, lct, b, op, tile, stage, s_tw + P * NTW);
       __syncthreads();  // the next prime reuses the transform panel
     }
@@ -1151,9 +1154,11 @@ __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int 
   if (rows > R) rows = R;
   uint2* stage = reinterpret_cast<uint2*>(smem + M * sm_len(LGR2) * CT);
   stage_operand(ov, stage, rows, lct, LGC, tile << lct);
+  const int q0 = gridDim.y > 1 ? job.p0 + (int)blockIdx.y : job.p0;  // as k_col_fwd_all
+  const int qn = gridDim.y > 1 ? 1 : job.pn;
   sfor<kNumPrimes>([&](auto pc) {
     constexpr int P = decltype(pc)::value;
-    if (P >= job.p0 && P < job.p0 + job.pn) {
+    if (P >= q0 && P < q0 + qn) {
       colm_fwd_body<P, M, LGR2, LGC, true>(job, tab, lct, b, op, tile, stage, rows);
       __syncthreads();  // the next prime reuses the transform panel
     }

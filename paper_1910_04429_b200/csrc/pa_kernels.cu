@@ -1272,6 +1272,8 @@ static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
   return nullptr;
 }
 
+constexpr unsigned kSMs = 148;  // B200
+
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
   if (job.m == 1 && job.lgR == 0) {
@@ -1307,7 +1309,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     const size_t ntw = (size_t)job.np << (pp.slo[0] + pp.rs[0]);  // staged first-pass twiddles
     const size_t sma = smc + (size_t)rows * (1u << lct) * 8 + ntw * 8;
     prof::Scope ps_("k_col_fwd", st);
-    col_fwd_all_kernel(job.lgR, job.lgC)<<<ctas_all, threads, sma, st>>>(job, tab, lct);
+    // fewer CTAs than two waves' worth of SMs (a few blocks): one prime per CTA
+    const unsigned gy = ctas_all < 2 * kSMs ? (unsigned)job.pn : 1u;
+    col_fwd_all_kernel(job.lgR, job.lgC)<<<dim3(ctas_all, gy), threads, sma, st>>>(job, tab, lct);
   } else if (job.m > 1 && fwd_all) {
     const int dl = 1;  // half-width tiles: the staged rows fit with 4-5 CTAs per SM (measured)
     const int lcta = lct - dl < 2 ? 2 : lct - dl;
@@ -1316,7 +1320,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     const size_t sma = (size_t)job.m * sm_len(job.lgR) * (1u << lcta) * 4 + (size_t)rows * (1u << lcta) * 8;
     const unsigned ctas = (1u << (job.lgC - lcta)) * 2u * (unsigned)job.batch;
     prof::Scope ps_("k_col_fwd", st);
-    colm_fwd_all_kernel(job.m, job.lgR, job.lgC)<<<ctas, cf_threads, sma, st>>>(job, tab, lcta);
+    const unsigned gy = ctas < 2 * kSMs ? (unsigned)job.pn : 1u;  // as above
+    colm_fwd_all_kernel(job.m, job.lgR, job.lgC)<<<dim3(ctas, gy), cf_threads, sma, st>>>(job, tab,
+                                                                                          lcta);
   } else {
     prof::Scope ps_("k_col_fwd", st);
     // ~32 MiB of operand words per chunk (L2-resident across the prime sweeps)
