@@ -174,7 +174,7 @@ class HashEngine:
     def hash_seeded_host(self, x: torch.Tensor, rng_seed, first_index: int = 0,
                          out: torch.Tensor | None = None, streams: int = 3,
                          chunk: int | None = None, join_in: bool = True,
-                         join_out: bool = True, seed_budget: int = 2 << 30,
+                         join_out: bool = True, seed_budget: int = 4 << 30,
                          protocol: str = "run_pa") -> torch.Tensor:
         """run_pa's step end to end: key blocks x from (pinned) host memory, block
         first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
@@ -206,7 +206,7 @@ class HashEngine:
         per_block = 2 * self.nbytes
         win = max(chunk, min(-(-b // chunk) * chunk,
                              (max(chunk, seed_budget // per_block // 4) // chunk) * chunk))
-        nbuf = max(2, min(16, seed_budget // (per_block * win)))
+        nbuf = max(2, min(32, seed_budget // (per_block * win)))
         wins = self._seed_windows(nbuf, win)
         cur = torch.cuda.current_stream(self.device)
         if join_in:
