@@ -41,7 +41,11 @@ __attribute__((target("avx2"))) uint64_t digits_to_bytes_avx2(const uint32_t* di
   }
   return g;
 }
-const bool kHasAvx2 = __builtin_cpu_supports("avx2");
+// (evaluated while the library loads, before main: run the CPU detection first)
+const bool kHasAvx2 = [] {
+  __builtin_cpu_init();
+  return __builtin_cpu_supports("avx2") != 0;
+}();
 #endif
 }  // namespace
 
