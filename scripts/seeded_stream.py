@@ -9,6 +9,7 @@ sys.path.insert(0, ".")
 from paper_1910_04429_b200.batch import HashEngine  # noqa: E402
 
 n, r, B, K = (int(float(v)) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (1e6, 5e5, 1024, 10)))
+CH = int(sys.argv[5]) if len(sys.argv) > 5 else None  # hashing chunk (blocks per launch)
 nb = (n + 7) // 8
 eng = HashEngine(n, r, max_batch=B)
 px = torch.randint(0, 256, (B, nb), dtype=torch.uint8).pin_memory()
@@ -28,7 +29,7 @@ def timed(fn):
 
 def streamed():
     for i in range(K):
-        eng.hash_seeded_host(px, 0, 0, hout, join_in=i == 0, join_out=False)
+        eng.hash_seeded_host(px, 0, 0, hout, join_in=i == 0, join_out=False, chunk=CH)
     eng.join()
 
 
@@ -45,6 +46,6 @@ res = {
     "hash_only_ms_per_step": timed(lambda: [eng.hash_device(dx, c, d, dout) for _ in range(K)]) / K,
 }
 res = {k: round(v, 3) for k, v in res.items()}
-res.update(n=n, r=r, B=B, K=K, mbps_streamed=round(B * n / res["streamed_ms_per_step"] / 1e3, 1),
+res.update(n=n, r=r, B=B, K=K, chunk=CH, mbps_streamed=round(B * n / res["streamed_ms_per_step"] / 1e3, 1),
            mbps_one_call=round(B * n / res["one_call_ms_per_step"] / 1e3, 1))
 print(json.dumps(res), flush=True)
