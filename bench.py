@@ -522,6 +522,7 @@ def roofline_obj(prof: dict, n: int, r: int, blocks: int, workload: str | None,
              "alg_Tops": round(mdl["ops"] / avg_s / 1e12, 2)}
         if name in kcnt:
             k["issue_frac"] = round(kcnt[name]["inst"] * 32 / avg_s / 1e12 / pk["int_tops"], 4)
+            k["fmaheavy_frac_ncu"] = kcnt[name].get("pipe_fmaheavy")
         kernels[name] = k
     if not prof:
         return None, kernels
@@ -549,7 +550,10 @@ def roofline_obj(prof: dict, n: int, r: int, blocks: int, workload: str | None,
                            "%d blocks/launch)" % (dom, workload, blocks),
                 "ncu": {x: kc.get(x) for x in ("issue_active", "pipe_alu", "pipe_fma",
                                                 "pipe_fmaheavy", "duration_ms", "sm_mhz")},
-                "hbm": hbm, "algorithmic": alg}
+                "hbm": hbm, "algorithmic": alg,
+                "binding": {"resource": "fma-heavy pipe (IMAD, IMAD.HI, IMAD.WIDE: every "
+                                        "integer multiply; 64 lanes/clk/SM)",
+                            "frac_ncu": kc.get("pipe_fmaheavy")}}
     else:  # no matching capture committed: report the algorithmic HBM fraction only
         roof = dict(hbm, bound="hbm", kernel=dom, traffic=None, algorithmic=alg,
                     note="no ncu counts for this workload/batch: int fraction unavailable")
