@@ -99,3 +99,22 @@ def test_compress_over_int_digits_matches_oracle():
             assert got == int.from_bytes(want, "little"), (n, r, kind)
             if kind == "identity" and r == n:
                 assert got == x
+
+
+def test_digit_path_in_the_three_prime_mode():
+    # n beyond the five-prime bound (32-bit coefficients over three primes): the
+    # Python-int digit path equals the byte path, itself pinned to the oracle in
+    # test_gpu_configs (max sizes); ragged n and r around digit / word edges
+    from paper_1910_04429_b200 import _native
+
+    rng = random.Random(31)
+    n = 121_295_104 + 1_000_003
+    assert _native.plan_width(n) == (32, 3)
+    x, c, d = rng.getrandbits(n), rng.getrandbits(n) | 1, rng.getrandbits(n)
+    nb = (n + 7) // 8
+    for r in (n, n - 29, 77_777_777):
+        got = pab.compress(pab.BitBlock(x, n),
+                           pab.HashSeed(c=pab.BigNat(c), d=pab.BigNat(d), alpha=n), r).value
+        raw = _native.hash_host(x.to_bytes(nb, "little"), c.to_bytes(nb, "little"),
+                                d.to_bytes(nb, "little"), n, r)
+        assert got == int.from_bytes(raw, "little"), r
