@@ -789,12 +789,19 @@ def main():
 
     import torch
 
-    torch.cuda.set_device(local_rank)
+    # development switches for exercising the N-rank path on a one-GPU box: every rank
+    # on cuda:0 (PAB_BENCH_SAME_DEVICE=1) with host-side collectives (PAB_BENCH_BACKEND=gloo)
+    dev = 0 if os.environ.get("PAB_BENCH_SAME_DEVICE") == "1" else local_rank
+    backend = os.environ.get("PAB_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as tdist
 
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
     solo = rank == 0 and world == 1
 
