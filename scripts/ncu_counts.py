@@ -4,6 +4,8 @@ On the GPU box, under ncu (after the same command ran clean without it):
     python scripts/ncu_counts.py run C2        # bench's C2 batch: 1024 blocks per launch
     python scripts/ncu_counts.py run C5        # 64 blocks of n=1e8 per launch
     python scripts/ncu_counts.py run C4        # one n=1e8 block
+    python scripts/ncu_counts.py run C3        # 64 blocks of n=1e7 per launch
+    python scripts/ncu_counts.py run C1        # one n=1e6 block
 Each run hashes the workload's batch twice (the second pass is the one kept).
 Here, from the CSVs ncu wrote (--csv --log-file):
     python scripts/ncu_counts.py parse gpurun_out/ncu_counts_C2.csv ... -o profiles/ncu_counts.json
@@ -20,7 +22,8 @@ METRICS = ("smsp__inst_executed.sum,smsp__thread_inst_executed.sum,"
            "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
            "smsp__cycles_elapsed.avg.per_second")
 SHAPES = {"C2": (1_000_000, 500_000, 1024), "C5": (100_000_000, 50_000_000, 64),
-          "C4": (100_000_000, 50_000_000, 1)}
+          "C4": (100_000_000, 50_000_000, 1), "C3": (10_000_000, 2_000_000, 64),
+          "C1": (1_000_000, 500_000, 1)}
 # CUDA kernel name -> the launcher's profile name (bench.py's kernel table)
 FAMILY = (("k_col_fwd", "k_col_fwd"), ("k_colm_fwd", "k_col_fwd"), ("k_col_inv", "k_col_inv"),
           ("k_colm_inv", "k_col_inv"), ("k_carry", "k_carry"), ("k_row", "k_row"),
