@@ -1347,8 +1347,11 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     prof::Scope ps_("k_row", st);
     const ConvKernel rt = tab.tw4 ? conv_for(job.lgC).row_tw4 : nullptr;
     const ConvKernel rk = rt ? rt : row_kernel(job.lgC, false);
-    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), narrow ? 64 : 128, smr, st>>>(job, tab,
-                                                                                      lnr);
+    // a few blocks (under two waves of CTAs): 256 threads per CTA, so each CTA's
+    // passes finish in fewer task rounds (latency rather than throughput)
+    const long long ctas = (long long)job.batch * (R >> lnr) * job.pn;
+    const int rthreads = ctas < 2 * (long long)kSMs ? 256 : (narrow ? 64 : 128);
+    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), rthreads, smr, st>>>(job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
