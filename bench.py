@@ -551,13 +551,34 @@ def roofline_obj(prof: dict, n: int, r: int, blocks: int, workload: str | None,
                 "ncu": {x: kc.get(x) for x in ("issue_active", "pipe_alu", "pipe_fma",
                                                 "pipe_fmaheavy", "duration_ms", "sm_mhz")},
                 "hbm": hbm, "algorithmic": alg,
-                "binding": {"resource": "fma-heavy pipe (IMAD, IMAD.HI, IMAD.WIDE: every "
-                                        "integer multiply; 64 lanes/clk/SM)",
-                            "frac_ncu": kc.get("pipe_fmaheavy")}}
+                "binding": dict({"resource": "fma-heavy pipe (IMAD, IMAD.HI, IMAD.WIDE: every "
+                                             "integer multiply; 64 lanes/clk/SM)",
+                                 "frac_ncu": kc.get("pipe_fmaheavy")},
+                                **mix_ceiling(ach / pk["int_tops"]))}
     else:  # no matching capture committed: report the algorithmic HBM fraction only
         roof = dict(hbm, bound="hbm", kernel=dom, traffic=None, algorithmic=alg,
                     note="no ncu counts for this workload/batch: int fraction unavailable")
     return roof, kernels
+
+
+def mix_ceiling(issue_frac: float) -> dict:
+    """The issue fraction a stream of Shoup butterflies can reach at all: measured
+    per-instruction pipe costs (scripts/pipe_rates.cu -> profiles/r2/pipe_rates.json):
+    IMAD 2 clk per warp per SMSP, IMAD.HI and IMAD.WIDE 4, so a Shoup product holds the
+    FMA pipe 8 clk and a 6-instruction butterfly cannot issue above 6/8 of the slots."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "pipe_rates.json")) as f:
+            pr = json.load(f)
+        ceil_frac = 6.0 * pr["shoup_products"]
+    except (OSError, ValueError, KeyError):
+        return {}
+    return {"pipe_clk_per_warp_instr": {k: round(1.0 / pr[k], 2) for k in
+                                        ("imad", "imad_hi", "imad_wide", "iadd3", "viaddmnmx", "lop3")},
+            "shoup_product_clk": round(1.0 / pr["shoup_products"], 2),
+            "butterfly_clk_ideal_stream": round(1.0 / pr["butterflies"], 2),
+            "issue_ceiling_butterfly_mix": round(ceil_frac, 4),
+            "issue_frac_of_ceiling": round(issue_frac / ceil_frac, 4),
+            "src": "profiles/r2/pipe_rates.json (scripts/pipe_rates.cu on this B200 pool)"}
 
 
 def step_roofline(n: int, r: int, blocks: int, ms_step: float, sm_mhz: float | None,
