@@ -418,16 +418,46 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         eng.join(st)
         e1.record(st)
         torch.cuda.synchronize()
-        s_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
+        c_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
         assert torch.equal(sout, first_out), "seeded e2e keys differ from device-resident keys"
+        per_call = {"value": round(bits_step / (c_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
+                    "ms_per_step": round(c_ms, 4),
+                    "scope": "one hash_seeded_host call per step (the step's seeds repeated), "
+                             "calls streamed; expansion and hashing share the GPU"}
+        # the e2e: the K steps as ONE call over K x per_rank blocks (a key file handed to
+        # the engine, as run_pa does): block j's seed is seeds[0] + j, x repeats the step's
+        # key blocks.  Calls this size expand each seed window on the hashing stream right
+        # before its chunks (the two do not share the SMs); H2D and D2H overlap both.
+        pbig = px.repeat(steps, 1).pin_memory()
+        sbig = torch.empty((steps * per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
+        eng.hash_seeded_host(pbig, None, seeds[0], sbig, protocol="bench")  # warm-up (buffers)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0.record(st)
+        eng.hash_seeded_host(pbig, None, seeds[0], sbig, protocol="bench")
+        e1.record(st)
+        torch.cuda.synchronize()
+        s_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
+        assert torch.equal(sbig[:per_rank], first_out), \
+            "seeded e2e keys differ from device-resident keys"
+        vc, vd = torch.empty_like(dx), torch.empty_like(dx)
+        for t in range(1, steps):  # later steps: seeds expanded and hashed device-resident
+            eng.seed_device(None, seeds[0] + t * per_rank, per_rank, vc, vd, protocol="bench")
+            want = eng.hash_device(dx, vc, vd).cpu()
+            assert torch.equal(sbig[t * per_rank:(t + 1) * per_rank], want), \
+                "seeded e2e keys of step %d differ from the device-resident path" % t
+        del pbig, vc, vd
         e2e = {"value": round(bits_step / (s_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
                "h2d_bytes_per_step": per_rank * eng.nbytes,
                "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(s_ms, 4),
-               "scope": "HashEngine.hash_seeded_host(protocol='bench'): pinned x -> GPU, each "
-                        "block's (c, d) = gen_seed(n, derive_block_seed(s, n)) expanded on the "
-                        "GPU (SHAKE-256), keys -> pinned host, consecutive steps streamed; keys "
-                        "bit-identical to the device-resident leg",
-               "xcd": e2e_xcd}
+               "scope": "HashEngine.hash_seeded_host(protocol='bench'), one call over the "
+                        "%d steps' %d blocks: pinned x -> GPU, block j's (c, d) = gen_seed(n, "
+                        "derive_block_seed(s0 + j, n)) expanded on the GPU (SHAKE-256), keys -> "
+                        "pinned host; the first step's keys bit-identical to the device-resident "
+                        "leg, the rest to the device-resident path on the same seeds"
+                        % (steps, steps * per_rank),
+               "per_step_calls": per_call, "xcd": e2e_xcd}
     clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
 
     e2e_seeded = run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) \
@@ -462,27 +492,29 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     import torch
     from paper_1910_04429_b200 import pa
 
-    first = rank * per_rank
-    hout = torch.empty((per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
-    for _ in range(max(1, args.warmup)):
-        eng.hash_seeded_host(px, 0, first, hout, streams=3)
+    # one call over the K steps' blocks, as run_pa hands a rank its whole shard: rank k
+    # hashes run_pa blocks k*K*B .. (k+1)*K*B - 1 (x repeats the step's key blocks)
+    first = rank * per_rank * steps
+    total = per_rank * steps
+    pbig = px.repeat(steps, 1).pin_memory()
+    hout = torch.empty((total, eng.rbytes), dtype=torch.uint8, pin_memory=True)
+    eng.hash_seeded_host(pbig, 0, first, hout, streams=3)  # warm-up (buffers)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for i in range(steps):
-        eng.hash_seeded_host(px, 0, first, hout, streams=3, join_in=i == 0, join_out=False)
-    eng.join(st)
+    eng.hash_seeded_host(pbig, 0, first, hout, streams=3)
     e1.record(st)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
-    # spot check: two blocks against host-derived seeds through the device path
+    # spot check: blocks against host-derived seeds through the device path
     nb = eng.nbytes
-    idx = [0, per_rank - 1]
-    dx = px[idx].cuda()
-    dc = torch.empty((2, nb), dtype=torch.uint8)
+    idx = [0, per_rank - 1, total - 1]
+    dx = pbig[idx].cuda()
+    del pbig
+    dc = torch.empty((len(idx), nb), dtype=torch.uint8)
     dd = torch.empty_like(dc)
     for j, i in enumerate(idx):
         sd = pa.gen_seed(n, pa.derive_block_seed(0, first + i))
@@ -491,8 +523,9 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     want = eng.hash_device(dx, dc.cuda(), dd.cuda()).cpu()
     assert torch.equal(hout[idx], want), "run_pa e2e keys differ from host-derived seeds"
     return {"value": round(bits_step / (ms * 1e-3) / 1e6, 1), "unit": "Mbps",
-            "scope": "run_pa: x pinned host -> GPU, (c, d) = gen_seed(n, derive_block_seed(0, i))"
-                     " expanded on the GPU (SHAKE-256), keys -> host",
+            "scope": "run_pa: one call over the %d steps' blocks; x pinned host -> GPU, (c, d) = "
+                     "gen_seed(n, derive_block_seed(0, i)) expanded on the GPU (SHAKE-256), "
+                     "keys -> host" % steps,
             "h2d_bytes_per_step": per_rank * nb, "d2h_bytes_per_step": per_rank * eng.rbytes,
             "ms_per_step": round(ms, 4)}
 

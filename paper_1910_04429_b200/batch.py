@@ -22,6 +22,11 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+# hash_seeded_host: smallest seed window (blocks) expanded on the hashing stream
+# (2 XOF streams per block: >= 8192 lane pairs per launch, throughput-bound)
+kExclusiveMin = 4096
+
+
 class HashEngine:
     """Hash batches of n-bit blocks down to r bits on one CUDA device.
 
@@ -175,7 +180,7 @@ class HashEngine:
                          out: torch.Tensor | None = None, streams: int = 3,
                          chunk: int | None = None, join_in: bool = True,
                          join_out: bool = True, seed_budget: int = 4 << 30,
-                         protocol: str = "run_pa") -> torch.Tensor:
+                         protocol: str = "run_pa", exclusive: bool | None = None) -> torch.Tensor:
         """run_pa's step end to end: key blocks x from (pinned) host memory, block
         first_index + j hashed with gen_seed(n, derive_block_seed(rng_seed, first_index + j))
         derived on the GPU (only x crosses PCIe); protocol "bench" derives the
@@ -191,6 +196,16 @@ class HashEngine:
         the expansion of the windows after it.  Hand a whole key file (shard) to
         one call: the expansion latency is then paid once per `seed_budget` of
         blocks, not once per chunk.  join_in / join_out as in hash_host.
+
+        Big calls at small n take another schedule (`exclusive`, default: chosen by
+        size).  Expansion and hashing share an SM badly: the Keccak warps keep the
+        ALU pipe the butterflies also need busy, and a 1024-block step of both at
+        n = 1e6 measures 2.6-2.8 ms against 0.57 + 1.66 ms one after the other
+        (scripts/seed_hash_corun.py).  When `seed_budget` holds one window of at
+        least kExclusiveMin blocks (enough XOF streams for the expansion to be
+        throughput-bound instead of one chain long), the windows are expanded on
+        the hashing stream itself, each right before its chunks are hashed, so the
+        two never run together; the copies still overlap both.
         """
         b = x.shape[0]
         if out is None:
@@ -200,10 +215,25 @@ class HashEngine:
         s_in, s_comp, s_out = self._pipe_streams()
         bufs = self._io_buffers(nslots, chunk)
         ev = self._slot_events(nslots)
+        per_block = 2 * self.nbytes
+        # exclusive windows: long enough to be throughput-bound, short enough for the
+        # (nslots - 1) prefetched chunks to keep PCIe busy while one expands (measured at
+        # n = 1e6: 4096-block windows with 3 slots, 2.62 ms per 1024 blocks; 8192: 2.76)
+        xmax = seed_budget // per_block // chunk * chunk
+        xwin = min(xmax, max(kExclusiveMin, 2 * (nslots - 1) * chunk))
+        if exclusive is None:
+            exclusive = xwin >= kExclusiveMin and b >= kExclusiveMin
+        if exclusive and xwin >= chunk:
+            even = lambda k: -(-(-(-b // k)) // chunk) * chunk  # noqa: E731  (k windows of whole chunks)
+            nwin = max(1, b // xwin)
+            if even(nwin) > xmax:
+                nwin = -(-b // xmax)
+            xwin = even(nwin)
+            return self._hash_seeded_exclusive(x, rng_seed, first_index, out, nslots, chunk, xwin,
+                                               join_in, join_out, protocol)
         # windows of `win` blocks (whole hashing chunks) over `nbuf` rotating buffers:
         # up to nbuf windows -- of this call and of the calls queued after it --
         # expand concurrently
-        per_block = 2 * self.nbytes
         win = max(chunk, min(-(-b // chunk) * chunk,
                              (max(chunk, seed_budget // per_block // 4) // chunk) * chunk))
         nbuf = max(2, min(32, seed_budget // (per_block * win)))
@@ -252,6 +282,52 @@ class HashEngine:
         self._sw_next = (base + len(starts)) % nbuf
         self._slot_next = i % nslots
         if join_out:  # s_comp has waited for every seed window it used
+            self.join(cur)
+        return out
+
+    def _hash_seeded_exclusive(self, x, rng_seed, first_index, out, nslots, chunk, win,
+                               join_in, join_out, protocol):
+        """hash_seeded_host with each window of `win` blocks expanded on the hashing
+        stream right before its chunks (one (c, d) buffer, reused in stream order)."""
+        b = x.shape[0]
+        s_in, s_comp, s_out = self._pipe_streams()
+        bufs = self._io_buffers(nslots, chunk)
+        ev = self._slot_events(nslots)
+        if getattr(self, "_xw_win", 0) < win:
+            if getattr(self, "_xw_win", 0):
+                torch.cuda.synchronize(self.device)  # the old buffer may still be read
+            self._xw = tuple(torch.empty((win, self.nbytes), dtype=torch.uint8, device=self.device)
+                             for _ in range(2))
+            self._xw_win = win
+        sc, sd = self._xw
+        cur = torch.cuda.current_stream(self.device)
+        if join_in:
+            for s in (s_in, s_comp, s_out):
+                s.wait_stream(cur)
+        i = self._slot_next
+        for w0 in range(0, b, win):
+            self.seed_device(rng_seed, first_index + w0, min(win, b - w0), sc, sd, stream=s_comp,
+                             protocol=protocol)
+            for b0 in range(w0, min(b, w0 + win), chunk):
+                k = i % nslots
+                i += 1
+                dx, _, _, dout = bufs[k]
+                nb = min(chunk, b - b0)
+                s_in.wait_event(ev["comp"][k])       # slot k's inputs consumed
+                with torch.cuda.stream(s_in):
+                    dx[:nb].copy_(x[b0:b0 + nb], non_blocking=True)
+                    ev["in"][k].record(s_in)
+                s_comp.wait_event(ev["in"][k])
+                s_comp.wait_event(ev["out"][k])      # slot k's output drained
+                self.hash_device(dx[:nb], sc[b0 - w0:b0 - w0 + nb], sd[b0 - w0:b0 - w0 + nb],
+                                 dout[:nb], stream=s_comp)
+                ev["comp"][k].record(s_comp)
+                s_out.wait_event(ev["comp"][k])
+                with torch.cuda.stream(s_out):
+                    out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
+                    ev["out"][k].record(s_out)
+        self._slot_next = i % nslots
+        if join_out:
             self.join(cur)
         return out
 

@@ -164,6 +164,37 @@ def test_seed_windows_rotate_across_and_within_calls(budget_blocks):
             assert o[j].numpy().tobytes() == oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r)
 
 
+@pytest.mark.parametrize("exclusive", [True, None])
+def test_seed_windows_on_the_hashing_stream(exclusive):
+    # the exclusive schedule: each seed window expanded on the hashing stream right
+    # before its chunks (one buffer reused in stream order), forced on a small call
+    # with ragged windows and chosen by size on a call of >= kExclusiveMin blocks;
+    # keys equal the concurrent-window schedule's and the oracle's
+    from paper_1910_04429_b200 import batch
+
+    n, r = 4_160, 2_001
+    B = 23 if exclusive else batch.kExclusiveMin + 37
+    nb = (n + 7) // 8
+    rng = np.random.default_rng(B)
+    x = rng.integers(0, 256, size=(B, nb), dtype=np.uint8)
+    px = torch.from_numpy(x).pin_memory()
+    eng = HashEngine(n, r, max_batch=4 if exclusive else 512)
+    budget = 9 * 2 * nb if exclusive else 4 << 30  # forced: windows of 8 blocks (two chunks)
+    outs = [eng.hash_seeded_host(px, 6, f, join_in=i == 0, join_out=False, seed_budget=budget,
+                                 exclusive=exclusive) for i, f in enumerate((3, 90))]
+    eng.join()
+    torch.cuda.synchronize()
+    assert eng._xw_win == (8 if exclusive else 4608)  # even windows of whole chunks
+    ref = HashEngine(n, r, max_batch=64)
+    for f, o in zip((3, 90), outs):
+        want = ref.hash_seeded_host(px, 6, f, exclusive=False)
+        torch.cuda.synchronize()
+        assert torch.equal(o, want)
+        cs, ds = host_seeds(n, 6, f, B)
+        for j in (0, 7, 8, B - 1):
+            assert o[j].numpy().tobytes() == oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r)
+
+
 def test_bench_protocol_seeds_match_the_reference_workload():
     # pab_seed_expand_bench: block seed s -> gen_seed(n, derive_block_seed(s, n)), the
     # reference benchmark's (c, d) (pkg/src/modpa/bench.py:156; workloads.block_inputs)
