@@ -52,11 +52,18 @@ __device__ __forceinline__ OpView op_view(const ConvJob& job, int op, int b) {
   return v;
 }
 // coefficient (lo, hi) -> residue in [0, 2p)
+// The low word needs no multiply: 2^32 < 6p for every prime, so it is below 6p and
+// two subtract-and-min steps by 2p bring it (or its sum with the high word's Shoup
+// product, which stays below 2^32) into [0, 2p).  An IMAD.HI holds the FMA pipe 4
+// clk and an IMAD 2 (profiles/r2/pipe_rates.json); these are ALU-pipe ops.
 template <int P>
 __device__ __forceinline__ u32 coef_red(u32 lo, u32 hi, int cw) {
-  const u32 a = shoup(lo, 1u, PK<P>::one_sh, PK<P>::p);
-  if (cw == 1) return a;
-  return red(a + shoup(hi, PK<P>::r32, PK<P>::r32_sh, PK<P>::p), PK<P>::two_p);
+  static_assert(6ull * kPrimes[P] > (1ull << 32), "low word must be below 6p");
+  const u32 a = red(lo, PK<P>::two_p);  // < max(2p, 2^32 - 2p) < 4p
+  if (cw == 1) return red(a, PK<P>::two_p);
+  // a + s < 2^32: a < 2p gives < 4p, else a < 2^32 - 2p and s < 2p
+  const u32 s = a + shoup(hi, PK<P>::r32, PK<P>::r32_sh, PK<P>::p);
+  return red(red(s, PK<P>::two_p), PK<P>::two_p);
 }
 // the two words of 64-bit coefficient gi (cw = 2): one 8-byte load on 8-byte
 // aligned rows, else two 4-byte loads; the last coefficient of an odd word
