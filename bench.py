@@ -428,6 +428,19 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         # the engine, as run_pa does): block j's seed is seeds[0] + j, x repeats the step's
         # key blocks.  Calls this size expand each seed window on the hashing stream right
         # before its chunks (the two do not share the SMs); H2D and D2H overlap both.
+        from paper_1910_04429_b200 import batch as _batch
+        one_call = (steps * per_rank >= _batch.kExclusiveMin and
+                    (4 << 30) // (2 * eng.nbytes) >= _batch.kExclusiveMin)
+    if n <= 10_000_000 and seeds == list(range(seeds[0], seeds[0] + per_rank)) and not one_call:
+        # calls too small (or blocks too long) for the exclusive seed schedule: the
+        # streamed per-step calls are the e2e
+        e2e = dict(per_call, h2d_bytes_per_step=per_rank * eng.nbytes,
+                   d2h_bytes_per_step=per_rank * eng.rbytes, xcd=e2e_xcd)
+        e2e["scope"] = ("HashEngine.hash_seeded_host(protocol='bench'): pinned x -> GPU, each "
+                        "block's (c, d) = gen_seed(n, derive_block_seed(s, n)) expanded on the "
+                        "GPU (SHAKE-256), keys -> pinned host, consecutive steps streamed; keys "
+                        "bit-identical to the device-resident leg")
+    elif n <= 10_000_000 and seeds == list(range(seeds[0], seeds[0] + per_rank)):
         pbig = px.repeat(steps, 1).pin_memory()
         sbig = torch.empty((steps * per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
         eng.hash_seeded_host(pbig, None, seeds[0], sbig, protocol="bench")  # warm-up (buffers)
@@ -492,20 +505,32 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     import torch
     from paper_1910_04429_b200 import pa
 
-    # one call over the K steps' blocks, as run_pa hands a rank its whole shard: rank k
-    # hashes run_pa blocks k*K*B .. (k+1)*K*B - 1 (x repeats the step's key blocks)
-    first = rank * per_rank * steps
-    total = per_rank * steps
-    pbig = px.repeat(steps, 1).pin_memory()
+    from paper_1910_04429_b200 import batch as _batch
+
+    # calls big enough for the exclusive seed schedule: one call over the K steps' blocks,
+    # as run_pa hands a rank its whole shard (rank k hashes run_pa blocks k*K*B ..
+    # (k+1)*K*B - 1, x repeats the step's key blocks); else one streamed call per step
+    one_call = (steps * per_rank >= _batch.kExclusiveMin and
+                (4 << 30) // (2 * eng.nbytes) >= _batch.kExclusiveMin)
+    reps = steps if one_call else 1
+    first = rank * per_rank * reps
+    total = per_rank * reps
+    pbig = px.repeat(reps, 1).pin_memory() if one_call else px
     hout = torch.empty((total, eng.rbytes), dtype=torch.uint8, pin_memory=True)
-    eng.hash_seeded_host(pbig, 0, first, hout, streams=3)  # warm-up (buffers)
+    for _ in range(1 if one_call else max(1, args.warmup)):
+        eng.hash_seeded_host(pbig, 0, first, hout, streams=3)  # warm-up (buffers)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    eng.hash_seeded_host(pbig, 0, first, hout, streams=3)
+    if one_call:
+        eng.hash_seeded_host(pbig, 0, first, hout, streams=3)
+    else:
+        for i in range(steps):
+            eng.hash_seeded_host(pbig, 0, first, hout, streams=3, join_in=i == 0, join_out=False)
+        eng.join(st)
     e1.record(st)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
@@ -523,9 +548,10 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     want = eng.hash_device(dx, dc.cuda(), dd.cuda()).cpu()
     assert torch.equal(hout[idx], want), "run_pa e2e keys differ from host-derived seeds"
     return {"value": round(bits_step / (ms * 1e-3) / 1e6, 1), "unit": "Mbps",
-            "scope": "run_pa: one call over the %d steps' blocks; x pinned host -> GPU, (c, d) = "
+            "scope": "run_pa: %s; x pinned host -> GPU, (c, d) = "
                      "gen_seed(n, derive_block_seed(0, i)) expanded on the GPU (SHAKE-256), "
-                     "keys -> host" % steps,
+                     "keys -> host" % ("one call over the %d steps' blocks" % steps if one_call
+                                       else "one streamed call per step"),
             "h2d_bytes_per_step": per_rank * nb, "d2h_bytes_per_step": per_rank * eng.rbytes,
             "ms_per_step": round(ms, 4)}
 
