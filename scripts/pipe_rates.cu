@@ -24,6 +24,9 @@ enum Mode {
   M_WIDE_IADD2,   // 1 WIDE : 2 IADD3
   M_MONT,         // Montgomery product (WIDE, LO, HI + 3 alu)
   M_SHOUP_WIDE,   // 1 HI : 1 LOP3
+  M_BFLY_ASM,     // the butterfly with its two-operand add pinned as add.u32 (stays IADD3)
+  M_IADD3_IMM,    // three-operand IADD3 (register + register + immediate)
+  M_SUB,          // two-register subtract
   M_COUNT
 };
 
@@ -99,6 +102,20 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, uint32_t seed) {
         uint32_t mh = __umulhi(m, p);
         y = hi + mh + (lo != 0u ? 1u : 0u);
         x = min(y + x, y + x - tp);
+      } else if (MODE == M_BFLY_ASM) {
+        uint32_t s;
+        asm volatile("add.u32 %0, %1, %2;" : "=r"(s) : "r"(x), "r"(y));
+        s = min(s, s - tp);
+        uint32_t d = x - y + tp;
+        uint32_t q = __umulhi(d, wp);
+        y = d * w - q * p;
+        x = s;
+      } else if (MODE == M_IADD3_IMM) {
+        x = x + y + 0x1234u;
+        y = y + x + 0x77u;
+      } else if (MODE == M_SUB) {
+        asm volatile("sub.u32 %0, %0, %1;" : "+r"(x) : "r"(w));
+        asm volatile("sub.u32 %0, %0, %1;" : "+r"(y) : "r"(wp));
       } else if (MODE == M_SHOUP_WIDE) {  // 1 HI : 1 LOP3
         asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x) : "r"(wp));
         asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y) : "r"(w), "r"(wp));
@@ -162,6 +179,9 @@ int main() {
   printf(", \"wide_plus_2iadd_groups\": %.4f", run<M_WIDE_IADD2>(sms, mhz, 1));
   printf(", \"mont_products\": %.4f", run<M_MONT>(sms, mhz, 1));
   printf(", \"hi_plus_lop3_pairs\": %.4f", run<M_SHOUP_WIDE>(sms, mhz, 1));
+  printf(", \"butterflies_add_pinned\": %.4f", run<M_BFLY_ASM>(sms, mhz, 1));
+  printf(", \"iadd3_three_operand\": %.4f", run<M_IADD3_IMM>(sms, mhz, 2));
+  printf(", \"sub_two_register\": %.4f", run<M_SUB>(sms, mhz, 2));
   printf("}\n");
   return 0;
 }
