@@ -46,3 +46,50 @@ def test_run_bench_on_gpu(scope):
     assert [r.block_size for r in recs] == [50_000, 100_000]
     assert all(r.algorithm == benchrun.ALGORITHM and r.throughput_mbps > 0 for r in recs)
     assert bench_csv(recs).startswith("block_size,algorithm,trials,elapsed_ms,throughput_mbps")
+
+
+@pytest.mark.gpu
+def test_run_bench_rounds_compute_the_reference_keys(monkeypatch):
+    # run_bench only returns timings; spy on what each scope's timed call computed and
+    # check it against the oracle (pipeline, device) or Python's own product (multiply)
+    import oracle
+    from paper_1910_04429_b200 import batch
+
+    sizes = (50_000, 1_000_000)
+    rounds, products, device = [], [], []
+    real_round, real_mul, real_hash = benchrun.pa.pa_round, benchrun.mul, batch.HashEngine.hash_device
+
+    def spy_round(block, params, seed, enforce=True):
+        out = real_round(block, params, seed, enforce=enforce)
+        rounds.append((block, params, seed, out))
+        return out
+
+    def spy_mul(a, b, *args, **kw):
+        out = real_mul(a, b, *args, **kw)
+        products.append((a, b, out))
+        return out
+
+    def spy_hash(self, x, c, d, *args, **kw):
+        out = real_hash(self, x, c, d, *args, **kw)
+        device.append((self.n, self.r, x, c, d, out))
+        return out
+
+    monkeypatch.setattr(benchrun.pa, "pa_round", spy_round)
+    monkeypatch.setattr(benchrun, "mul", spy_mul)
+    monkeypatch.setattr(batch.HashEngine, "hash_device", spy_hash)
+    for scope in ("pipeline", "multiply", "device"):
+        run_bench(RunConfig(sizes=sizes, trials=2), scope=scope)
+    assert len(rounds) == 4 and len(products) == 4 and len(device) == 8
+    for block, params, seed, out in rounds:
+        nb = (params.n + 7) // 8
+        want = oracle.compress(block.value.to_bytes(nb, "little"), seed.c.value.to_bytes(nb, "little"),
+                               seed.d.value.to_bytes(nb, "little"), params.n, params.r)
+        assert out.n == params.r and out.value == int.from_bytes(want, "little")
+    for a, b, out in products:
+        assert out.value == a.value * b.value
+    import torch
+    torch.cuda.synchronize()
+    for n, r, x, c, d, out in device:
+        want = oracle.compress(bytes(x[0].cpu().numpy()), bytes(c[0].cpu().numpy()),
+                               bytes(d[0].cpu().numpy()), n, r)
+        assert bytes(out[0].cpu().numpy()) == want

@@ -163,3 +163,29 @@ def test_run_pa_gpu_long_seed_material(tmp_path):
                          out_path=str(out)), **kw)
         outs.append(out.read_bytes())
     assert outs[0] == outs[1] and len(outs[0]) == 3 * 256
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,blocks,ratio", [(1_000_000, 40, 0.5), (4_160, 4_200, 0.25)])
+def test_run_pa_gpu_at_config_size(tmp_path, n, blocks, ratio):
+    # a key file of C2-size blocks (and one big enough for the seed windows to run on
+    # the hashing stream: >= 4096 blocks), every key against the oracle on host-derived
+    # seeds -- what the reference's run_pa computes block by block (bench.py:256-262)
+    rng = np.random.default_rng(blocks)
+    nb = n // 8
+    data = rng.integers(0, 256, size=blocks * nb, dtype=np.uint8)
+    key, out = tmp_path / "key.bin", tmp_path / "out.bin"
+    key.write_bytes(data.tobytes())
+    res = run_pa(RunConfig(sizes=(n,), ratio=ratio, rng_seed=77, in_path=str(key),
+                           out_path=str(out)))
+    r = max(1, int(ratio * n))
+    rb = (r + 7) // 8
+    got = out.read_bytes()
+    assert res.blocks == blocks and len(got) == blocks * rb
+    x = data.reshape(blocks, nb)
+    step = 1 if n >= 1_000_000 else 97
+    for i in list(range(0, blocks, step)) + [blocks - 1]:
+        s = pa.gen_seed(n, pa.derive_block_seed(77, i))
+        want = oracle.compress(x[i].tobytes(), s.c.value.to_bytes(nb, "little"),
+                               s.d.value.to_bytes(nb, "little"), n, r)
+        assert got[i * rb:(i + 1) * rb] == want, i
