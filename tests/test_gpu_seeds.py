@@ -173,7 +173,7 @@ def test_seed_windows_on_the_hashing_stream(exclusive):
     from paper_1910_04429_b200 import batch
 
     n, r = 4_160, 2_001
-    B = 23 if exclusive else batch.kExclusiveMin + 37
+    B = 23 if exclusive else batch.kExclusiveMin + 300  # last chunk of 300: hashed in quarters
     nb = (n + 7) // 8
     rng = np.random.default_rng(B)
     x = rng.integers(0, 256, size=(B, nb), dtype=np.uint8)
