@@ -441,14 +441,25 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
                         "GPU (SHAKE-256), keys -> pinned host, consecutive steps streamed; keys "
                         "bit-identical to the device-resident leg")
     elif n <= 10_000_000 and seeds == list(range(seeds[0], seeds[0] + per_rank)):
-        pbig = px.repeat(steps, 1).pin_memory()
+        # (at most kCallSteps steps per call, so the pinned key file stays a few GB
+        # whatever --steps is: K steps = ceil(K / kCallSteps) calls back to back)
+        groups = call_groups(steps)
+        pbig = px.repeat(max(groups), 1).pin_memory()
         sbig = torch.empty((steps * per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
-        eng.hash_seeded_host(pbig, None, seeds[0], sbig, protocol="bench")  # warm-up (buffers)
+
+        def calls():
+            t = 0
+            for g in groups:
+                eng.hash_seeded_host(pbig[:g * per_rank], None, seeds[0] + t * per_rank,
+                                     sbig[t * per_rank:(t + g) * per_rank], protocol="bench")
+                t += g
+
+        calls()  # warm-up (buffers)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         e0.record(st)
-        eng.hash_seeded_host(pbig, None, seeds[0], sbig, protocol="bench")
+        calls()
         e1.record(st)
         torch.cuda.synchronize()
         s_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
@@ -464,8 +475,10 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         e2e = {"value": round(bits_step / (s_ms * 1e-3) / 1e6, 1), "unit": "Mbps",
                "h2d_bytes_per_step": per_rank * eng.nbytes,
                "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(s_ms, 4),
+               "calls": len(groups),
                "scope": "HashEngine.hash_seeded_host(protocol='bench'), one call over the "
-                        "%d steps' %d blocks: pinned x -> GPU, block j's (c, d) = gen_seed(n, "
+                        "%d steps' %d blocks (at most 32 steps per call): pinned x -> GPU, "
+                        "block j's (c, d) = gen_seed(n, "
                         "derive_block_seed(s0 + j, n)) expanded on the GPU (SHAKE-256), keys -> "
                         "pinned host; the first step's keys bit-identical to the device-resident "
                         "leg, the rest to the device-resident path on the same seeds"
@@ -497,6 +510,15 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
             "inputs": (xs, cs, ds), "chunk": eng.chunk}
 
 
+kCallSteps = 32  # steps handed to one hash_seeded_host call in the e2e legs
+
+
+def call_groups(steps: int) -> list[int]:
+    """K steps as ceil(K / kCallSteps) calls of nearly equal size."""
+    k = -(-steps // kCallSteps)
+    return [steps // k + (1 if i < steps % k else 0) for i in range(k)]
+
+
 def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict:
     """run_pa's scope end to end (pkg/src/modpa/bench.py:256-262): the key blocks
     from pinned host memory, block i hashed with gen_seed(n, derive_block_seed(0, i))
@@ -512,7 +534,8 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     # (k+1)*K*B - 1, x repeats the step's key blocks); else one streamed call per step
     one_call = (steps * per_rank >= _batch.kExclusiveMin and
                 (4 << 30) // (2 * eng.nbytes) >= _batch.kExclusiveMin)
-    reps = steps if one_call else 1
+    groups = call_groups(steps) if one_call else [1]
+    reps = max(groups)
     first = rank * per_rank * reps
     total = per_rank * reps
     pbig = px.repeat(reps, 1).pin_memory() if one_call else px
@@ -526,7 +549,8 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     if one_call:
-        eng.hash_seeded_host(pbig, 0, first, hout, streams=3)
+        for g in groups:  # (each call re-hashes the file's first g steps)
+            eng.hash_seeded_host(pbig[:g * per_rank], 0, first, hout[:g * per_rank], streams=3)
     else:
         for i in range(steps):
             eng.hash_seeded_host(pbig, 0, first, hout, streams=3, join_in=i == 0, join_out=False)
