@@ -210,6 +210,17 @@ __device__ __forceinline__ u32 coef_staged(const uint2* stage, int row, int t, i
   return coef_red<P>(w.x, w.y, cw);
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-stream-serialization attribute may become resident while its
+// predecessor in the stream still runs; pdl_wait() blocks until that grid has
+// completed and its writes are visible, pdl_launch() lets this grid's own
+// successor start launching.  Both are no-ops under an ordinary launch.
+// Every kernel of the hash calls them first, so completion orders transitively.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // conv kernels run one prime per grid index IDX (primes p0 .. p0 + pn - 1).  Kernels
 // without cross-prime data reuse (row, inverse column) put the prime in the
 // slowest grid dimension so CTAs resident together run the same prime's
@@ -489,6 +500,7 @@ __device__ __forceinline__ void row_body(const ConvJob& job, const PlanTables& t
 
 template <int LGC, bool SMALL, bool TW4 = false>
 __global__ void __launch_bounds__(256) k_row(ConvJob job, PlanTables tab, int lnr) {
+  pdl_enter();
 #define PAB_B(P_) row_body<P_, LGC, SMALL, TW4>(job, tab, lnr);
   PAB_PRIME_SWITCH(PAB_B, job.p0 + (int)blockIdx.z)
 #undef PAB_B
@@ -1078,6 +1090,7 @@ template <int M, int LGR2, int LGC>
 #define PAB_COLM3_FWD_REGS 64
 #endif
 __global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   constexpr int lct = col_lct_rows((long long)M << LGR2, LGC);  // compile-time tile width
   if (lct_in != lct) __trap();
   const FwdIdx ix = fwd_idx(job, lct);
@@ -1087,6 +1100,7 @@ __global__ void __maxnreg__(M == 3 ? PAB_COLM3_FWD_REGS : 48) k_colm_fwd(ConvJob
 }
 template <int M, int LGR2, int LGC>
 __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   constexpr int lct = col_lct_rows((long long)M << LGR2, LGC);  // compile-time tile width
   if (lct_in != lct) __trap();
 #define PAB_B(P_) colm_inv_body<P_, M, LGR2, LGC>(job, tab, lct);
@@ -1096,6 +1110,7 @@ __global__ void __launch_bounds__(512) k_colm_inv(ConvJob job, PlanTables tab, i
 
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   constexpr int LCT = col_lct(LGR, LGC);
   if (lct_in != LCT) __trap();  // the launcher's width is this constant
   const FwdIdx ix = fwd_idx(job, LCT);
@@ -1109,6 +1124,7 @@ __global__ void __launch_bounds__(256, 5) k_col_fwd(ConvJob job, PlanTables tab,
 // plus the stage (rows x CT x 8 bytes).
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   extern __shared__ u32 smem[];
   constexpr int lct = col_lct(LGR, LGC);
   if (lct_in != lct) __trap();  // the launcher's width is this constant
@@ -1145,6 +1161,7 @@ __global__ void __launch_bounds__(256) k_col_fwd_all(ConvJob job, PlanTables tab
 // column DFT reads them from smem.
 template <int M, int LGR2, int LGC>
 __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   extern __shared__ u32 smem[];
   // half-width tiles (the launcher's lcta), compile-time
   constexpr int lct = col_lct_rows((long long)M << LGR2, LGC) - 1 < 2
@@ -1174,6 +1191,7 @@ __global__ void __maxnreg__(48) k_colm_fwd_all(ConvJob job, PlanTables tab, int 
 
 template <int LGR, int LGC>
 __global__ void __launch_bounds__(256) k_col_inv(ConvJob job, PlanTables tab, int lct_in) {
+  pdl_enter();
   constexpr int LCT = col_inv_lct(LGR, LGC);
   if (lct_in != LCT) __trap();  // the launcher's width is this constant
 #define PAB_B(P_) col_inv_body<P_, LGR, LGC, LCT>(job, tab, LCT);

@@ -776,6 +776,7 @@ __device__ __forceinline__ u32 carry_tile(const ConvJob& job, CarrySmem& sm, int
 // barrier stalls behind warp 0's long look-back walks).
 template <int CW>
 __global__ void __launch_bounds__(kCarryThreads) k_carry_lb(ConvJob job) {
+  pdl_enter();
   __shared__ CarrySmem sm;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
@@ -829,6 +830,7 @@ __device__ __forceinline__ u32 res_or0(const u32* __restrict__ res, long long L,
 #define PAB_WIDE_MINB 6
 #endif
 __global__ void __launch_bounds__(kWThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob job) {
+  pdl_enter();
   __shared__ WideSmem sm;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) sm.tile = atomicAdd(&job.tile_ctr[b], 1u);
@@ -1098,6 +1100,7 @@ __global__ void __launch_bounds__(kWThreads, PAB_WIDE_MINB) k_carry_wide(ConvJob
 // One CTA per block walking its tiles in order (many blocks): no inter-CTA waits.
 template <int CW>
 __global__ void __launch_bounds__(kCarryThreads) k_carry_seq(ConvJob job) {
+  pdl_enter();
   __shared__ CarrySmem sm;
   const int b = blockIdx.y;
   u32 c = 0;
@@ -1274,6 +1277,34 @@ static ConvKernel col_kernel(int lgR, int lgC, bool inv) {
 
 constexpr unsigned kSMs = 148;  // B200
 
+// Launch a kernel whose predecessor in the stream is another kernel of the same
+// hash, as its programmatic dependent when `small` (pdl_enter() in
+// conv_kernels.cuh): its launch and prologue overlap the predecessor's tail.
+// Only launches of a few blocks gain (one 1e6-bit block: 0.0405 -> 0.0368 ms per
+// hash); at full batches the early-resident dependents cost 2-4% (C2 1.647 ->
+// 1.676 ms, 16 x 1e8 3.42 -> 3.57 ms), so those launch the ordinary way.
+// PAB_PDL=0 / 1 (development switch) forces it off / on for every launch.
+template <class... KArgs, class... Args>
+static void launch_dep(bool small, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  static const int force = [] {
+    const char* e = getenv("PAB_PDL");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool pdl = force < 0 ? small : force != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
+}
+
 void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
   const int threads = 256;
   if (job.m == 1 && job.lgR == 0) {
@@ -1351,7 +1382,8 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     // passes finish in fewer task rounds (latency rather than throughput)
     const long long ctas = (long long)job.batch * (R >> lnr) * job.pn;
     const int rthreads = ctas < 2 * (long long)kSMs ? 256 : (narrow ? 64 : 128);
-    rk<<<dim3(job.batch, (unsigned)(R >> lnr), job.pn), rthreads, smr, st>>>(job, tab, lnr);
+    launch_dep(ctas < 2 * (long long)kSMs, rk, dim3(job.batch, (unsigned)(R >> lnr), job.pn),
+               dim3(rthreads), smr, st, job, tab, lnr);
   }
   {
     prof::Scope ps_("k_col_inv", st);
@@ -1360,8 +1392,9 @@ void launch_conv(const ConvJob& job, const PlanTables& tab, cudaStream_t st) {
     const int lci = job.m == 1 ? col_inv_lct(job.lgR, job.lgC) : lct;
     const int xi = lct - lci;
     const size_t smi = (size_t)job.m * sm_len(job.lgR) * (1u << lci) * 4;
-    ci<<<dim3(1u << (job.lgC - lci), job.batch, job.pn), ct_threads >> xi, smi, st>>>(job, tab,
-                                                                                   lci);
+    const long long ctas = ((long long)job.batch * job.pn) << (job.lgC - lci);
+    launch_dep(ctas < 2 * (long long)kSMs, ci, dim3(1u << (job.lgC - lci), job.batch, job.pn),
+               dim3(ct_threads >> xi), smi, st, job, tab, lci);
   }
 }
 
@@ -1384,7 +1417,8 @@ void launch_carry(const ConvJob& job, cudaStream_t st) {
   if (job.cw == 2 && force != 1 && force != 2) {  // wide layout (PAB_CARRY_MODE=seq|lb: the old ones)
     ConvJob jw = job;
     jw.tiles = (int)((job.nT + kWTileWords - 1) / kWTileWords);
-    k_carry_wide<<<dim3(job.batch, jw.tiles), kWThreads, 0, st>>>(jw);
+    launch_dep((long long)job.batch * jw.tiles < 2 * (long long)kSMs, k_carry_wide,
+               dim3(job.batch, jw.tiles), dim3(kWThreads), 0, st, jw);
     return;
   }
   ConvJob jo = job;
