@@ -447,11 +447,12 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         pbig = px.repeat(max(groups), 1).pin_memory()
         sbig = torch.empty((steps * per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
 
-        def calls():
+        def calls():  # streamed: a call's head overlaps the tail of the one before
             t = 0
-            for g in groups:
+            for i, g in enumerate(groups):
                 eng.hash_seeded_host(pbig[:g * per_rank], None, seeds[0] + t * per_rank,
-                                     sbig[t * per_rank:(t + g) * per_rank], protocol="bench")
+                                     sbig[t * per_rank:(t + g) * per_rank], protocol="bench",
+                                     join_in=i == 0, join_out=i == len(groups) - 1)
                 t += g
 
         calls()  # warm-up (buffers)
@@ -549,8 +550,9 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     if one_call:
-        for g in groups:  # (each call re-hashes the file's first g steps)
-            eng.hash_seeded_host(pbig[:g * per_rank], 0, first, hout[:g * per_rank], streams=3)
+        for i, g in enumerate(groups):  # (each call re-hashes the file's first g steps)
+            eng.hash_seeded_host(pbig[:g * per_rank], 0, first, hout[:g * per_rank], streams=3,
+                                 join_in=i == 0, join_out=i == len(groups) - 1)
     else:
         for i in range(steps):
             eng.hash_seeded_host(pbig, 0, first, hout, streams=3, join_in=i == 0, join_out=False)

@@ -28,6 +28,17 @@ kExclusiveMin = 4096
 kTaperMin = 32  # the last chunk of an exclusive call is hashed in quarters of >= this many blocks
 
 
+def exclusive_windows(nchunks: int, target: int, cap: int) -> list[int]:
+    """Seed windows (in hashing chunks) of a call of `nchunks` chunks on the exclusive
+    schedule: as even as possible, none above `target` chunks (a longer expansion
+    starves the copies) -- except a call of up to 1.5 targets, which is one window
+    (two short windows would each be one chain long) -- and none above `cap`."""
+    if nchunks <= min(cap, target + target // 2):
+        return [nchunks]
+    k = -(-nchunks // min(target, cap))
+    return [nchunks // k + (1 if i < nchunks % k else 0) for i in range(k)]
+
+
 class HashEngine:
     """Hash batches of n-bit blocks down to r bits on one CUDA device.
 
@@ -225,13 +236,10 @@ class HashEngine:
         if exclusive is None:
             exclusive = xwin >= kExclusiveMin and b >= kExclusiveMin
         if exclusive and xwin >= chunk:
-            even = lambda k: -(-(-(-b // k)) // chunk) * chunk  # noqa: E731  (k windows of whole chunks)
-            nwin = max(1, b // xwin)
-            if even(nwin) > xmax:
-                nwin = -(-b // xmax)
-            xwin = even(nwin)
-            return self._hash_seeded_exclusive(x, rng_seed, first_index, out, nslots, chunk, xwin,
-                                               join_in, join_out, protocol)
+            wins = exclusive_windows(-(-b // chunk), xwin // chunk, xmax // chunk)
+            return self._hash_seeded_exclusive(x, rng_seed, first_index, out, nslots, chunk,
+                                               [w * chunk for w in wins], join_in, join_out,
+                                               protocol)
         # windows of `win` blocks (whole hashing chunks) over `nbuf` rotating buffers:
         # up to nbuf windows -- of this call and of the calls queued after it --
         # expand concurrently
@@ -286,11 +294,12 @@ class HashEngine:
             self.join(cur)
         return out
 
-    def _hash_seeded_exclusive(self, x, rng_seed, first_index, out, nslots, chunk, win,
+    def _hash_seeded_exclusive(self, x, rng_seed, first_index, out, nslots, chunk, wins,
                                join_in, join_out, protocol):
-        """hash_seeded_host with each window of `win` blocks expanded on the hashing
-        stream right before its chunks (one (c, d) buffer, reused in stream order)."""
+        """hash_seeded_host with each window (`wins`: blocks per window) expanded on the
+        hashing stream right before its chunks (one (c, d) buffer, reused in stream order)."""
         b = x.shape[0]
+        win = max(wins)
         s_in, s_comp, s_out = self._pipe_streams()
         bufs = self._io_buffers(nslots, chunk)
         ev = self._slot_events(nslots)
@@ -306,11 +315,13 @@ class HashEngine:
             for s in (s_in, s_comp, s_out):
                 s.wait_stream(cur)
         i = self._slot_next
-        for w0 in range(0, b, win):
-            self.seed_device(rng_seed, first_index + w0, min(win, b - w0), sc, sd, stream=s_comp,
+        w0 = 0
+        for wlen in wins:
+            w1 = min(b, w0 + wlen)
+            self.seed_device(rng_seed, first_index + w0, w1 - w0, sc, sd, stream=s_comp,
                              protocol=protocol)
-            pieces = [(b0, min(chunk, b - b0)) for b0 in range(w0, min(b, w0 + win), chunk)]
-            if join_out and w0 + win >= b and pieces[-1][1] >= 4 * kTaperMin:
+            pieces = [(b0, min(chunk, w1 - b0)) for b0 in range(w0, w1, chunk)]
+            if join_out and w1 >= b and pieces[-1][1] >= 4 * kTaperMin:
                 # the call's last chunk in quarters: after the last H2D only a quarter's
                 # hashing and D2H remain (measured at C2: 2.85 -> 0.8 ms of drain per call)
                 b0, nb = pieces.pop()
@@ -333,6 +344,7 @@ class HashEngine:
                 with torch.cuda.stream(s_out):
                     out[b0:b0 + nb].copy_(dout[:nb], non_blocking=True)
                     ev["out"][k].record(s_out)
+            w0 = w1
         self._slot_next = i % nslots
         if join_out:
             self.join(cur)
