@@ -157,3 +157,22 @@ def test_digit_level_int_byte_conversions():
         assert pab.export_block(blk, order) == raw
     with pytest.raises(ValueError, match="beyond"):
         pab.import_block(b"\xff" * 5000, 5000 * 8 - 3)
+
+
+def test_exclusive_seed_windows_cover_the_call():
+    # hash_seeded_host's exclusive schedule: windows (in hashing chunks) cover the call
+    # exactly, stay at or under the target (or the cap), and are as even as possible;
+    # a call of up to 1.5 targets is one window
+    from paper_1910_04429_b200.batch import exclusive_windows
+
+    assert exclusive_windows(20, 4, 16) == [4, 4, 4, 4, 4]
+    assert exclusive_windows(25, 4, 16) == [4, 4, 4, 4, 3, 3, 3]
+    assert exclusive_windows(9, 8, 1000) == [9]
+    assert exclusive_windows(13, 8, 1000) == [7, 6]
+    assert exclusive_windows(6, 2, 2) == [2, 2, 2]
+    for n in range(1, 200):
+        for target, cap in ((4, 16), (8, 5), (3, 3), (16, 1000)):
+            w = exclusive_windows(n, target, cap)
+            assert sum(w) == n and min(w) >= 1 and max(w) - min(w) <= 1
+            assert max(w) <= cap or n <= cap
+            assert len(w) == 1 or max(w) <= min(target, cap)
