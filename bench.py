@@ -445,14 +445,15 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         # whatever --steps is: K steps = ceil(K / kCallSteps) calls back to back)
         groups = call_groups(steps)
         pbig = px.repeat(max(groups), 1).pin_memory()
-        sbig = torch.empty((steps * per_rank, eng.rbytes), dtype=torch.uint8, pin_memory=True)
+        sbig = torch.empty((max(groups) * per_rank, eng.rbytes), dtype=torch.uint8,
+                           pin_memory=True)
 
-        def calls():  # streamed: a call's head overlaps the tail of the one before
+        def calls(grp=groups):  # streamed: a call's head overlaps the tail of the one before
             t = 0
-            for i, g in enumerate(groups):
+            for i, g in enumerate(grp):  # (every call's keys land in the same host buffer)
                 eng.hash_seeded_host(pbig[:g * per_rank], None, seeds[0] + t * per_rank,
-                                     sbig[t * per_rank:(t + g) * per_rank], protocol="bench",
-                                     join_in=i == 0, join_out=i == len(groups) - 1)
+                                     sbig[:g * per_rank], protocol="bench",
+                                     join_in=i == 0, join_out=i == len(grp) - 1)
                 t += g
 
         calls()  # warm-up (buffers)
@@ -464,10 +465,12 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         e1.record(st)
         torch.cuda.synchronize()
         s_ms = max_over_ranks(e0.elapsed_time(e1) / steps, dist)
+        calls(groups[:1])  # the first call once more, its keys checked step by step
+        torch.cuda.synchronize()
         assert torch.equal(sbig[:per_rank], first_out), \
             "seeded e2e keys differ from device-resident keys"
         vc, vd = torch.empty_like(dx), torch.empty_like(dx)
-        for t in range(1, steps):  # later steps: seeds expanded and hashed device-resident
+        for t in range(1, groups[0]):  # later steps: seeds expanded and hashed device-resident
             eng.seed_device(None, seeds[0] + t * per_rank, per_rank, vc, vd, protocol="bench")
             want = eng.hash_device(dx, vc, vd).cpu()
             assert torch.equal(sbig[t * per_rank:(t + 1) * per_rank], want), \
@@ -481,8 +484,9 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
                         "%d steps' %d blocks (at most 32 steps per call): pinned x -> GPU, "
                         "block j's (c, d) = gen_seed(n, "
                         "derive_block_seed(s0 + j, n)) expanded on the GPU (SHAKE-256), keys -> "
-                        "pinned host; the first step's keys bit-identical to the device-resident "
-                        "leg, the rest to the device-resident path on the same seeds"
+                        "pinned host; checked on the first call: its first step's keys "
+                        "bit-identical to the device-resident leg, its other steps' to the "
+                        "device-resident path on the same seeds"
                         % (steps, steps * per_rank),
                "per_step_calls": per_call, "xcd": e2e_xcd}
     clocks = clk.stop()  # sampled across the device-resident and the e2e timed regions
