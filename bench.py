@@ -345,7 +345,12 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
 
     clk = ClockSampler(torch.cuda.current_device())
     clk.start()
-    ms, prof = time_device(eng, dx, dc, dd, dout, steps, args.warmup, dist)
+    # K steps with a CUDA event pair around every kernel (the per-kernel durations of the
+    # roofline), then the timed region proper: the same K steps without those events (8
+    # event records per step stand between the launches and cost ~1% at C2, ~40% at C1)
+    ms_ev, prof = time_device(eng, dx, dc, dd, dout, steps, args.warmup, dist)
+    ms_ev = max_over_ranks(ms_ev / steps, dist)
+    ms, _ = time_device(eng, dx, dc, dd, dout, steps, 1, dist, profile=False)
     ms_step = max_over_ranks(ms / steps, dist)
     bits_step = world * per_rank * n
     value = bits_step / (ms_step * 1e-3) / 1e6
@@ -509,7 +514,8 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
                           "ms_per_step": round(ms_r, 4), "steps": k,
                           "step_roofline_frac": sr["frac"]})
             del e_r, o_r
-    return {"ms_step": ms_step, "value": value, "prof": prof, "clocks": clocks, "e2e": e2e,
+    return {"ms_step": ms_step, "ms_step_events": ms_ev, "value": value, "prof": prof,
+            "clocks": clocks, "e2e": e2e,
             "e2e_seeded": e2e_seeded, "ratio_sweep": sweep, "out": first_out,
             "per_rank": per_rank, "n": n, "r": r, "eng": eng, "seeds": seeds, "steps": steps,
             "inputs": (xs, cs, ds), "chunk": eng.chunk}
@@ -748,12 +754,21 @@ def leg_line(args, cfg, res, world, cpu=None) -> dict:
     return {
         "value": round(res["value"], 1), "unit": "Mbps", "ms_per_step": round(res["ms_step"], 4),
         "steps": res["steps"],
+        "with_kernel_events": {
+            "ms_per_step": round(res["ms_step_events"], 4),
+            "value": round(res["value"] * res["ms_step"] / res["ms_step_events"], 1),
+            "note": "the same K steps, run right before the timed region, with a CUDA event "
+                    "pair around every kernel launch: the source of `kernels` and of the "
+                    "roofline's launch durations"},
         "config": {"workload": cfg["name"], "n": n, "r": r, "blocks_per_rank": per_rank,
                    "blocks_per_launch": res["chunk"],
                    "block_seeds": "rank*%d + 0..%d" % (per_rank, per_rank - 1),
                    "parallelism": f"blocks sharded by index over {world} GPU(s), no collective",
                    "l2": "inputs %.0f MB/rank > 126 MB L2 (no flush needed)"
-                         % (3 * per_rank * ((n + 7) // 8) / 1e6)},
+                         % (3 * per_rank * ((n + 7) // 8) / 1e6),
+                   "timing": "K steps between CUDA events on the launching stream, barrier + "
+                             "synchronize on both sides, max over ranks; the per-kernel event "
+                             "pairs run over the K steps before (with_kernel_events)"},
         "e2e": res["e2e"], "e2e_run_pa": res["e2e_seeded"],
         "gpu_launches": sum(v[0] for v in res["prof"].values()),
         "roofline": roof,
