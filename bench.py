@@ -453,12 +453,11 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
         sbig = torch.empty((max(groups) * per_rank, eng.rbytes), dtype=torch.uint8,
                            pin_memory=True)
 
-        def calls(grp=groups):  # streamed: a call's head overlaps the tail of the one before
-            t = 0
-            for i, g in enumerate(grp):  # (every call's keys land in the same host buffer)
+        def calls(grp=groups):  # each a synchronous call: the engine hands it to the C-ABI
+            t = 0               # pipeline, pab_hash_seeded_host_bench (host buffers in, keys out)
+            for g in grp:       # (every call's keys land in the same host buffer)
                 eng.hash_seeded_host(pbig[:g * per_rank], None, seeds[0] + t * per_rank,
-                                     sbig[:g * per_rank], protocol="bench",
-                                     join_in=i == 0, join_out=i == len(grp) - 1)
+                                     sbig[:g * per_rank], protocol="bench")
                 t += g
 
         calls()  # warm-up (buffers)
@@ -485,7 +484,8 @@ def run_leg(args, cfg, rank, world, dist, steps) -> dict:
                "h2d_bytes_per_step": per_rank * eng.nbytes,
                "d2h_bytes_per_step": per_rank * eng.rbytes, "ms_per_step": round(s_ms, 4),
                "calls": len(groups),
-               "scope": "HashEngine.hash_seeded_host(protocol='bench'), one call over the "
+               "scope": "HashEngine.hash_seeded_host(protocol='bench') -> one C-ABI call "
+                        "(pab_hash_seeded_host_bench: host buffers in, keys out) over the "
                         "%d steps' %d blocks (at most 32 steps per call): pinned x -> GPU, "
                         "block j's (c, d) = gen_seed(n, "
                         "derive_block_seed(s0 + j, n)) expanded on the GPU (SHAKE-256), keys -> "
@@ -560,9 +560,9 @@ def run_pa_e2e(args, eng, px, per_rank, rank, n, bits_step, dist, steps) -> dict
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     if one_call:
-        for i, g in enumerate(groups):  # (each call re-hashes the file's first g steps)
-            eng.hash_seeded_host(pbig[:g * per_rank], 0, first, hout[:g * per_rank], streams=3,
-                                 join_in=i == 0, join_out=i == len(groups) - 1)
+        for g in groups:  # (each call re-hashes the file's first g steps; synchronous calls:
+            # the engine hands each to the C-ABI pipeline, pab_hash_seeded_host)
+            eng.hash_seeded_host(pbig[:g * per_rank], 0, first, hout[:g * per_rank])
     else:
         for i in range(steps):
             eng.hash_seeded_host(pbig, 0, first, hout, streams=3, join_in=i == 0, join_out=False)

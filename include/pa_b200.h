@@ -172,10 +172,26 @@ int pab_seed_expand_bench(uint64_t first_seed, uint32_t batch, uint64_t index, u
  * contiguous run of blocks): x = batch*ceil(n/8) host bytes (blocks first_index
  * .. first_index+batch-1 of the key file), seeds derived on the device by
  * pab_seed_expand, out = batch*ceil(r/8) host bytes.  Blocks until done.
+ * One call is the whole pipeline: the key blocks go host -> device in chunks of up
+ * to 1024 blocks on one stream, each seed window (4096 blocks where 4 GiB hold it)
+ * is expanded on the hashing stream right before its chunks, keys return on a
+ * third stream; three device slots.  Hand it a whole shard.  With x and out in
+ * pinned (page-locked) memory the copies overlap the hashing and x over PCIe is
+ * the bound (n = 1e6: 2.6 ms per 1024 blocks); pageable buffers are staged by the
+ * driver (about 7x slower there).
  */
 int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
                          int byte_order, const uint8_t* master, uint64_t master_len,
                          uint64_t first_index, uint8_t* out, int device);
+
+/*
+ * The same call on the reference benchmark protocol's seeds (pab_seed_expand_bench,
+ * pkg/src/modpa/bench.py:156): block j is hashed with
+ * gen_seed(n, derive_block_seed(first_seed + j, index)).
+ */
+int pab_hash_seeded_host_bench(const uint8_t* x, uint64_t n_bits, uint64_t r_bits,
+                               uint32_t batch, int byte_order, uint64_t first_seed,
+                               uint64_t index, uint8_t* out, int device);
 
 /*
  * Exact product of two naturals given as LSF byte strings (bignum.mul,

@@ -59,6 +59,9 @@ SIGNATURES = {
     "pab_hash_seeded_host": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint32, ctypes.c_int, _u8p, ctypes.c_uint64,
                                             ctypes.c_uint64, _u8p, ctypes.c_int]),
+    "pab_hash_seeded_host_bench": (ctypes.c_int, [_u8p, ctypes.c_uint64, ctypes.c_uint64,
+                                                  ctypes.c_uint32, ctypes.c_int, ctypes.c_uint64,
+                                                  ctypes.c_uint64, _u8p, ctypes.c_int]),
     "pab_mul_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint64]),
     "pab_mul": (ctypes.c_int, [_u8p, ctypes.c_uint64, _u8p, ctypes.c_uint64, _u8p, _u8p,
                                ctypes.c_size_t, _u8p]),
@@ -169,6 +172,14 @@ def seed_material(rng_seed) -> bytes:
             raise ValueError("integer seed material must be nonnegative")
         return rng_seed.to_bytes(max(1, (rng_seed.bit_length() + 7) // 8), "little")
     return bytes(rng_seed)
+
+
+def seed_material_fits(rng_seed) -> bool:
+    """The material fits the device expander's kernel parameter (MAX_SEED_MATERIAL bytes)."""
+    try:
+        return len(seed_material(rng_seed)) <= MAX_SEED_MATERIAL
+    except (TypeError, ValueError):
+        return False
 
 
 def hash_seeded_host(x: bytes, n: int, r: int, batch: int, rng_seed, first_index: int = 0,

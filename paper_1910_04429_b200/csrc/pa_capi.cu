@@ -169,6 +169,10 @@ struct HostCtx {  // cached buffers for the host-pointer entry points
   uint8_t* pinned = nullptr;      // pinned, mapped staging of the Python-int digit path
   uint8_t* pinned_dev = nullptr;
   size_t pinned_bytes = 0;
+  // pab_hash_seeded_host's pipeline: H2D / hashing / D2H streams and per-slot events
+  static constexpr int kSlots = 3;
+  cudaStream_t p_in = nullptr, p_comp = nullptr, p_out = nullptr;
+  cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
   std::mutex mu;
 };
 
@@ -887,44 +891,132 @@ int pab_seed_expand_bench(uint64_t first_seed, uint32_t batch, uint64_t index, u
   return PAB_OK;
 }
 
-int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
-                         int byte_order, const uint8_t* master, uint64_t master_len,
-                         uint64_t first_index, uint8_t* out, int device) {
+// Seed windows (in hashing chunks) of a call of `nchunks` chunks: as even as possible,
+// none above `target` chunks -- a longer expansion starves the copies -- except a call
+// of up to 1.5 targets, which is one window; none above `cap` (the seed budget).
+// (paper_1910_04429_b200/batch.py: exclusive_windows, the same policy.)
+static std::vector<u64> seed_windows(u64 nchunks, u64 target, u64 cap) {
+  if (cap < 1) cap = 1;
+  if (target < 1) target = 1;
+  const u64 one = target + target / 2 < cap ? target + target / 2 : cap;
+  if (nchunks <= one) return {nchunks};
+  const u64 t = target < cap ? target : cap;
+  const u64 k = ceil_div(nchunks, t);
+  std::vector<u64> w(k);
+  for (u64 i = 0; i < k; ++i) w[i] = nchunks / k + (i < nchunks % k ? 1 : 0);
+  return w;
+}
+
+// One call = the whole pipeline (the C counterpart of HashEngine.hash_seeded_host's
+// exclusive schedule): the key blocks go H2D chunk by chunk on one stream into
+// kSlots device slots, each seed window is expanded on the hashing stream right
+// before its chunks are hashed (expansion and hashing never share the SMs), keys
+// return D2H on a third stream; per-slot events order slot reuse.  With x and out in
+// pinned memory the copies overlap the hashing (n = 1e6: x over PCIe is the bound);
+// pageable buffers work too, at the speed the driver stages them.
+// bench_index >= 0: the reference benchmark protocol's seeds (pab_seed_expand_bench:
+// block j's seed is the integer first_index + j, label index bench_index)
+static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
+                            int byte_order, const uint8_t* master, uint64_t master_len,
+                            uint64_t first_index, long long bench_index, uint8_t* out,
+                            int device) {
   HashGeo g;
   int rc = hash_geo(n_bits, r_bits, &g);
   if (rc) return rc;
   if (batch == 0) return PAB_OK;
   if (!x || !out) return fail(PAB_EINVAL, "null pointer argument");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  if (first_index > ~0ull - batch) return fail(PAB_EINVAL, "block index overflows 64 bits");
   CK(cudaSetDevice(device), "cudaSetDevice");
   DevState* ds;
   if ((rc = ensure_device(device, &ds))) return rc;
   HostCtx& h = ds->host;
   std::lock_guard<std::mutex> lk(h.mu);
+  constexpr int kS = HostCtx::kSlots;
   const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
-  const u64 in_stride = round_up(nbytes, 16), out_stride = round_up(rbytes, 16);
-  u64 chunk = batch;
+  // rows the kernels can read and write in place stay packed (one contiguous copy per chunk)
+  const u64 in_stride = nbytes % 8 == 0 ? nbytes : round_up(nbytes, 16);
+  const u64 out_stride = rbytes % 4 == 0 ? rbytes : round_up(rbytes, 16);
+  // hashing chunks: at most 1024 blocks and ~2 GiB of transform workspace
+  u64 chunk = batch < 1024 ? batch : 1024;
   while (chunk > 1 && pab_hash_workspace_bytes(n_bits, (uint32_t)chunk) > ((size_t)2 << 30))
     chunk /= 2;
+  const u64 nchunks = ceil_div(batch, chunk);
+  // seed windows: 4096 blocks (8192 XOF streams: a throughput-bound launch) where the
+  // 4 GiB seed budget holds them, at least one chunk
+  const u64 cap = (((u64)4 << 30) / (2 * in_stride)) / chunk;
+  const u64 target = ceil_div(4096, chunk);
+  const std::vector<u64> wins = seed_windows(nchunks, target, cap);
+  u64 wmax = 0;
+  for (u64 w : wins) wmax = w > wmax ? w : wmax;
   const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, (uint32_t)chunk);
-  const size_t io_bytes = (size_t)batch * (3 * in_stride + out_stride);
-  if ((rc = host_ensure(h, ws_bytes, io_bytes))) return rc;
-  uint8_t* dx = h.dev_io;
-  uint8_t* dc = dx + batch * in_stride;
-  uint8_t* dd = dc + batch * in_stride;
-  uint8_t* dout = dd + batch * in_stride;
-  if ((rc = pab_seed_expand(master, master_len, first_index, batch, n_bits, byte_order, dc, dd,
-                            in_stride, h.stream)))
-    return rc;
-  CK(cudaMemcpy2DAsync(dx, in_stride, x, nbytes, nbytes, batch, cudaMemcpyHostToDevice, h.stream),
-     "H2D x");
-  rc = pab_hash_batch(dx, dc, dd, in_stride, n_bits, r_bits, batch, byte_order, dout, out_stride,
-                      h.ws, h.ws_bytes, h.stream);
-  if (rc) return rc;
-  CK(cudaMemcpy2DAsync(out, rbytes, dout, out_stride, rbytes, batch, cudaMemcpyDeviceToHost,
-                       h.stream),
-     "D2H out");
-  CK(cudaStreamSynchronize(h.stream), "synchronize");
+  const size_t slot_bytes = round_up(chunk * (in_stride + out_stride), 256);
+  const size_t seed_bytes = round_up(wmax * chunk * in_stride, 256);
+  if ((rc = host_ensure(h, ws_bytes, kS * slot_bytes + 2 * seed_bytes))) return rc;
+  if (!h.p_in) {
+    CK(cudaStreamCreateWithFlags(&h.p_in, cudaStreamNonBlocking), "stream");
+    CK(cudaStreamCreateWithFlags(&h.p_comp, cudaStreamNonBlocking), "stream");
+    CK(cudaStreamCreateWithFlags(&h.p_out, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < kS; ++k) {
+      CK(cudaEventCreateWithFlags(&h.ev_in[k], cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&h.ev_comp[k], cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&h.ev_out[k], cudaEventDisableTiming), "event");
+    }
+  }
+  uint8_t* dc = h.dev_io + kS * slot_bytes;
+  uint8_t* dd = dc + seed_bytes;
+  u64 b0 = 0, slot = 0;
+  for (u64 wlen : wins) {
+    const u64 w0 = b0;
+    const u64 w1 = w0 + wlen * chunk < batch ? w0 + wlen * chunk : batch;
+    rc = bench_index >= 0
+             ? pab_seed_expand_bench(first_index + w0, (uint32_t)(w1 - w0), (u64)bench_index,
+                                     n_bits, byte_order, dc, dd, in_stride, h.p_comp)
+             : pab_seed_expand(master, master_len, first_index + w0, (uint32_t)(w1 - w0), n_bits,
+                               byte_order, dc, dd, in_stride, h.p_comp);
+    if (rc) return rc;
+    for (; b0 < w1; b0 += chunk, ++slot) {
+      const int k = (int)(slot % kS);
+      const u64 nb = w1 - b0 < chunk ? w1 - b0 : chunk;
+      uint8_t* dx = h.dev_io + k * slot_bytes;
+      uint8_t* dout = dx + chunk * in_stride;
+      CK(cudaStreamWaitEvent(h.p_in, h.ev_comp[k], 0), "wait");  // slot k's inputs consumed
+      CK(cudaMemcpy2DAsync(dx, in_stride, x + b0 * nbytes, nbytes, nbytes, nb,
+                           cudaMemcpyHostToDevice, h.p_in), "H2D x");
+      CK(cudaEventRecord(h.ev_in[k], h.p_in), "record");
+      CK(cudaStreamWaitEvent(h.p_comp, h.ev_in[k], 0), "wait");
+      CK(cudaStreamWaitEvent(h.p_comp, h.ev_out[k], 0), "wait");  // slot k's keys drained
+      rc = pab_hash_batch(dx, dc + (b0 - w0) * in_stride, dd + (b0 - w0) * in_stride, in_stride,
+                          n_bits, r_bits, (uint32_t)nb, byte_order, dout, out_stride, h.ws,
+                          h.ws_bytes, h.p_comp);
+      if (rc) return rc;
+      CK(cudaEventRecord(h.ev_comp[k], h.p_comp), "record");
+      CK(cudaStreamWaitEvent(h.p_out, h.ev_comp[k], 0), "wait");
+      CK(cudaMemcpy2DAsync(out + b0 * rbytes, rbytes, dout, out_stride, rbytes, nb,
+                           cudaMemcpyDeviceToHost, h.p_out), "D2H out");
+      CK(cudaEventRecord(h.ev_out[k], h.p_out), "record");
+    }
+  }
+  CK(cudaStreamSynchronize(h.p_in), "synchronize");
+  CK(cudaStreamSynchronize(h.p_comp), "synchronize");
+  CK(cudaStreamSynchronize(h.p_out), "synchronize");
   return PAB_OK;
+}
+
+int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
+                         int byte_order, const uint8_t* master, uint64_t master_len,
+                         uint64_t first_index, uint8_t* out, int device) {
+  return seeded_host_impl(x, n_bits, r_bits, batch, byte_order, master, master_len, first_index,
+                          -1, out, device);
+}
+
+int pab_hash_seeded_host_bench(const uint8_t* x, uint64_t n_bits, uint64_t r_bits,
+                               uint32_t batch, int byte_order, uint64_t first_seed,
+                               uint64_t index, uint8_t* out, int device) {
+  if (index > (u64)LLONG_MAX) return fail(PAB_EINVAL, "label index beyond 2^63");
+  return seeded_host_impl(x, n_bits, r_bits, batch, byte_order, nullptr, 0, first_seed,
+                          (long long)index, out, device);
 }
 
 int pab_hash_host_split(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,

@@ -117,6 +117,62 @@ def test_hash_seeded_host_matches_oracle(n, r):
     assert [out[j].numpy().tobytes() for j in range(B)] == want
 
 
+@pytest.mark.parametrize("n,r,B,msf", [(4_160, 2_001, 7_173, False), (4_099, 4_099, 2_500, True),
+                                        (200_000, 64_000, 37, False)])
+def test_native_seeded_host_pipeline(n, r, B, msf):
+    # pab_hash_seeded_host: one C call = H2D / seed windows on the hashing stream / hash /
+    # D2H over three streams and three slots (several chunks, two seed windows, padded rows
+    # for byte-unaligned and MSF blocks); keys equal the engine's and the oracle's
+    order = _native.ORDER_MSF if msf else _native.ORDER_LSF
+    rng = np.random.default_rng(B)
+    nb, rb = (n + 7) // 8, (r + 7) // 8
+    x = rng.integers(0, 256, size=(B, nb), dtype=np.uint8)
+    if n % 8:
+        x[:, 0 if msf else -1] &= (1 << (n % 8)) - 1
+    got = _native.hash_seeded_host(x.tobytes(), n, r, B, 21, first_index=5, order=order)
+    assert len(got) == B * rb
+    eng = HashEngine(n, r, order=order, max_batch=512)
+    want = eng.hash_seeded_host(torch.from_numpy(x).pin_memory(), 21, first_index=5, exclusive=False)
+    torch.cuda.synchronize()
+    assert got == want.numpy().tobytes()
+    cs, ds = host_seeds(n, 21, 5, B, msf=msf)
+    for j in (0, 1023, 1024, B - 1):
+        if j < B:
+            assert got[j * rb:(j + 1) * rb] == oracle.compress(x[j].tobytes(), cs[j], ds[j], n, r,
+                                                               msf=msf), j
+    # a second call reuses the pipeline's slots and events
+    assert _native.hash_seeded_host(x[:3].tobytes(), n, r, 3, 21, first_index=5, order=order) == got[:3 * rb]
+
+
+@pytest.mark.parametrize("protocol", ["run_pa", "bench"])
+def test_engine_hands_synchronous_big_calls_to_the_native_pipeline(protocol):
+    # hash_seeded_host: a synchronous call of >= kExclusiveMin packed host blocks is one C call
+    # (native=None picks it); native=False keeps the Python-driven schedule; same keys
+    from paper_1910_04429_b200 import batch
+
+    n, r = 4_160, 1_999
+    B = batch.kExclusiveMin + 11
+    nb = n // 8
+    x = torch.from_numpy(np.random.default_rng(5).integers(0, 256, size=(B, nb), dtype=np.uint8))
+    eng = HashEngine(n, r, max_batch=256)
+    seed = None if protocol == "bench" else 12
+    calls = []
+    real = eng._hash_seeded_native
+    eng._hash_seeded_native = lambda *a: calls.append(1) or real(*a)
+    a = eng.hash_seeded_host(x.pin_memory(), seed, 7, protocol=protocol)
+    assert calls == [1]
+    b = eng.hash_seeded_host(x, seed, 7, protocol=protocol, native=False)  # pageable, Python path
+    c = eng.hash_seeded_host(x.pin_memory(), seed, 7, protocol=protocol, exclusive=False)
+    torch.cuda.synchronize()
+    assert calls == [1] and torch.equal(a, b) and torch.equal(a, c)
+    with pytest.raises(ValueError, match="native=True"):
+        eng.hash_seeded_host(x, seed, 7, protocol=protocol, native=True, join_out=False)
+    if protocol == "run_pa":
+        cs, ds = host_seeds(n, 12, 7, B)
+        for j in (0, B - 1):
+            assert a[j].numpy().tobytes() == oracle.compress(x[j].numpy().tobytes(), cs[j], ds[j], n, r)
+
+
 def test_streamed_calls_without_joins():
     # hash_host / hash_seeded_host chained with join_in / join_out off, one join() at the end
     n, r, B = 100_000, 30_001, 6
