@@ -97,7 +97,10 @@ int pab_hash_batch(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_
  * Host-buffer hash on `device` (the drop-in compress / pa_round path,
  * pkg/src/modpa/pa.py:175-217): copies x, c, d (batch*ceil(n/8) bytes each,
  * contiguous) host->device, hashes, copies batch*ceil(r/8) bytes back.
- * Uses a per-device cached workspace and stream; blocks until done.
+ * Batches run in chunks of up to 1024 blocks over three streams (H2D, hashing,
+ * D2H) and three device slots, so with pinned buffers the copies overlap the
+ * hashing; blocks of n <= 2048 bits take one kernel over mapped memory.
+ * Uses a per-device cached workspace; blocks until done.
  */
 int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
                   uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device);

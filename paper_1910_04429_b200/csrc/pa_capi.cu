@@ -684,6 +684,11 @@ static int host_ensure(HostCtx& h, size_t ws_bytes, size_t io_bytes) {
   return PAB_OK;
 }
 
+static int host_pipeline(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
+                         uint64_t r_bits, uint32_t batch, int byte_order, const uint8_t* master,
+                         uint64_t master_len, uint64_t first_index, long long bench_index,
+                         uint8_t* out, HostCtx& h);
+
 int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
                   uint64_t r_bits, uint32_t batch, int byte_order, uint8_t* out, int device) {
   HashGeo g;
@@ -719,32 +724,9 @@ int pab_hash_host(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t
     std::memcpy(out, h.mapped + 3 * batch * nbytes, batch * rbytes);
     return PAB_OK;
   }
-  const u64 in_stride = round_up(nbytes, 16), out_stride = round_up(rbytes, 16);
-  // at most ~2 GiB of transform workspace per chunk
-  u64 chunk = batch;
-  while (chunk > 1 && pab_hash_workspace_bytes(n_bits, (uint32_t)chunk) > ((size_t)2 << 30))
-    chunk /= 2;
-  const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, (uint32_t)chunk);
-  const size_t io_bytes = (size_t)batch * (3 * in_stride + out_stride);
-  if ((rc = host_ensure(h, ws_bytes, io_bytes))) return rc;
-  uint8_t* dx = h.dev_io;
-  uint8_t* dc = dx + batch * in_stride;
-  uint8_t* dd = dc + batch * in_stride;
-  uint8_t* dout = dd + batch * in_stride;
-  CK(cudaMemcpy2DAsync(dx, in_stride, x, nbytes, nbytes, batch, cudaMemcpyHostToDevice, h.stream),
-     "H2D x");
-  CK(cudaMemcpy2DAsync(dc, in_stride, c, nbytes, nbytes, batch, cudaMemcpyHostToDevice, h.stream),
-     "H2D c");
-  CK(cudaMemcpy2DAsync(dd, in_stride, d, nbytes, nbytes, batch, cudaMemcpyHostToDevice, h.stream),
-     "H2D d");
-  rc = pab_hash_batch(dx, dc, dd, in_stride, n_bits, r_bits, batch, byte_order, dout, out_stride,
-                      h.ws, h.ws_bytes, h.stream);
-  if (rc) return rc;
-  CK(cudaMemcpy2DAsync(out, rbytes, dout, out_stride, rbytes, batch, cudaMemcpyDeviceToHost,
-                       h.stream),
-     "D2H out");
-  CK(cudaStreamSynchronize(h.stream), "synchronize");
-  return PAB_OK;
+  if (!x || !c || !d || !out) return fail(PAB_EINVAL, "null pointer argument");
+  // chunks of blocks H2D / hashed / D2H on three streams over three device slots
+  return host_pipeline(x, c, d, n_bits, r_bits, batch, byte_order, nullptr, 0, 0, -1, out, h);
 }
 
 // Host copies of a few large buffers (the digit path at n ~ 1e8: 40 MB in, 7 MB
@@ -914,26 +896,18 @@ static std::vector<u64> seed_windows(u64 nchunks, u64 target, u64 cap) {
 // return D2H on a third stream; per-slot events order slot reuse.  With x and out in
 // pinned memory the copies overlap the hashing (n = 1e6: x over PCIe is the bound);
 // pageable buffers work too, at the speed the driver stages them.
-// bench_index >= 0: the reference benchmark protocol's seeds (pab_seed_expand_bench:
-// block j's seed is the integer first_index + j, label index bench_index)
-static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
-                            int byte_order, const uint8_t* master, uint64_t master_len,
-                            uint64_t first_index, long long bench_index, uint8_t* out,
-                            int device) {
-  HashGeo g;
-  int rc = hash_geo(n_bits, r_bits, &g);
-  if (rc) return rc;
-  if (batch == 0) return PAB_OK;
-  if (!x || !out) return fail(PAB_EINVAL, "null pointer argument");
-  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
-    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
-  if (first_index > ~0ull - batch) return fail(PAB_EINVAL, "block index overflows 64 bits");
-  CK(cudaSetDevice(device), "cudaSetDevice");
-  DevState* ds;
-  if ((rc = ensure_device(device, &ds))) return rc;
-  HostCtx& h = ds->host;
-  std::lock_guard<std::mutex> lk(h.mu);
+// The host-buffer pipeline (h.mu held, device current).  c != null: the members come
+// from the host with the key blocks (pab_hash_host); else they are expanded on the
+// device, bench_index >= 0 selecting the reference benchmark protocol's seeds
+// (pab_seed_expand_bench: block j's seed is the integer first_index + j, label index
+// bench_index) and bench_index < 0 run_pa's (pab_seed_expand).
+static int host_pipeline(const uint8_t* x, const uint8_t* c, const uint8_t* d, uint64_t n_bits,
+                         uint64_t r_bits, uint32_t batch, int byte_order, const uint8_t* master,
+                         uint64_t master_len, uint64_t first_index, long long bench_index,
+                         uint8_t* out, HostCtx& h) {
+  int rc;
   constexpr int kS = HostCtx::kSlots;
+  const bool seeded = c == nullptr;
   const u64 nbytes = ceil_div(n_bits, 8), rbytes = ceil_div(r_bits, 8);
   // rows the kernels can read and write in place stay packed (one contiguous copy per chunk)
   const u64 in_stride = nbytes % 8 == 0 ? nbytes : round_up(nbytes, 16);
@@ -944,15 +918,16 @@ static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, 
     chunk /= 2;
   const u64 nchunks = ceil_div(batch, chunk);
   // seed windows: 4096 blocks (8192 XOF streams: a throughput-bound launch) where the
-  // 4 GiB seed budget holds them, at least one chunk
+  // 4 GiB seed budget holds them, at least one chunk; host members: no windows
   const u64 cap = (((u64)4 << 30) / (2 * in_stride)) / chunk;
   const u64 target = ceil_div(4096, chunk);
-  const std::vector<u64> wins = seed_windows(nchunks, target, cap);
+  const std::vector<u64> wins = seeded ? seed_windows(nchunks, target, cap)
+                                       : std::vector<u64>{nchunks};
   u64 wmax = 0;
   for (u64 w : wins) wmax = w > wmax ? w : wmax;
   const size_t ws_bytes = pab_hash_workspace_bytes(n_bits, (uint32_t)chunk);
-  const size_t slot_bytes = round_up(chunk * (in_stride + out_stride), 256);
-  const size_t seed_bytes = round_up(wmax * chunk * in_stride, 256);
+  const size_t slot_bytes = round_up(chunk * ((seeded ? 1 : 3) * in_stride + out_stride), 256);
+  const size_t seed_bytes = seeded ? round_up(wmax * chunk * in_stride, 256) : 0;
   if ((rc = host_ensure(h, ws_bytes, kS * slot_bytes + 2 * seed_bytes))) return rc;
   if (!h.p_in) {
     CK(cudaStreamCreateWithFlags(&h.p_in, cudaStreamNonBlocking), "stream");
@@ -970,26 +945,35 @@ static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, 
   for (u64 wlen : wins) {
     const u64 w0 = b0;
     const u64 w1 = w0 + wlen * chunk < batch ? w0 + wlen * chunk : batch;
-    rc = bench_index >= 0
-             ? pab_seed_expand_bench(first_index + w0, (uint32_t)(w1 - w0), (u64)bench_index,
-                                     n_bits, byte_order, dc, dd, in_stride, h.p_comp)
-             : pab_seed_expand(master, master_len, first_index + w0, (uint32_t)(w1 - w0), n_bits,
-                               byte_order, dc, dd, in_stride, h.p_comp);
-    if (rc) return rc;
+    if (seeded) {
+      rc = bench_index >= 0
+               ? pab_seed_expand_bench(first_index + w0, (uint32_t)(w1 - w0), (u64)bench_index,
+                                       n_bits, byte_order, dc, dd, in_stride, h.p_comp)
+               : pab_seed_expand(master, master_len, first_index + w0, (uint32_t)(w1 - w0),
+                                 n_bits, byte_order, dc, dd, in_stride, h.p_comp);
+      if (rc) return rc;
+    }
     for (; b0 < w1; b0 += chunk, ++slot) {
       const int k = (int)(slot % kS);
       const u64 nb = w1 - b0 < chunk ? w1 - b0 : chunk;
       uint8_t* dx = h.dev_io + k * slot_bytes;
-      uint8_t* dout = dx + chunk * in_stride;
+      uint8_t* sc = seeded ? dc + (b0 - w0) * in_stride : dx + chunk * in_stride;
+      uint8_t* sd = seeded ? dd + (b0 - w0) * in_stride : dx + 2 * chunk * in_stride;
+      uint8_t* dout = dx + (seeded ? 1 : 3) * chunk * in_stride;
       CK(cudaStreamWaitEvent(h.p_in, h.ev_comp[k], 0), "wait");  // slot k's inputs consumed
       CK(cudaMemcpy2DAsync(dx, in_stride, x + b0 * nbytes, nbytes, nbytes, nb,
                            cudaMemcpyHostToDevice, h.p_in), "H2D x");
+      if (!seeded) {
+        CK(cudaMemcpy2DAsync(sc, in_stride, c + b0 * nbytes, nbytes, nbytes, nb,
+                             cudaMemcpyHostToDevice, h.p_in), "H2D c");
+        CK(cudaMemcpy2DAsync(sd, in_stride, d + b0 * nbytes, nbytes, nbytes, nb,
+                             cudaMemcpyHostToDevice, h.p_in), "H2D d");
+      }
       CK(cudaEventRecord(h.ev_in[k], h.p_in), "record");
       CK(cudaStreamWaitEvent(h.p_comp, h.ev_in[k], 0), "wait");
       CK(cudaStreamWaitEvent(h.p_comp, h.ev_out[k], 0), "wait");  // slot k's keys drained
-      rc = pab_hash_batch(dx, dc + (b0 - w0) * in_stride, dd + (b0 - w0) * in_stride, in_stride,
-                          n_bits, r_bits, (uint32_t)nb, byte_order, dout, out_stride, h.ws,
-                          h.ws_bytes, h.p_comp);
+      rc = pab_hash_batch(dx, sc, sd, in_stride, n_bits, r_bits, (uint32_t)nb, byte_order, dout,
+                          out_stride, h.ws, h.ws_bytes, h.p_comp);
       if (rc) return rc;
       CK(cudaEventRecord(h.ev_comp[k], h.p_comp), "record");
       CK(cudaStreamWaitEvent(h.p_out, h.ev_comp[k], 0), "wait");
@@ -1002,6 +986,27 @@ static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, 
   CK(cudaStreamSynchronize(h.p_comp), "synchronize");
   CK(cudaStreamSynchronize(h.p_out), "synchronize");
   return PAB_OK;
+}
+
+static int seeded_host_impl(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,
+                            int byte_order, const uint8_t* master, uint64_t master_len,
+                            uint64_t first_index, long long bench_index, uint8_t* out,
+                            int device) {
+  HashGeo g;
+  int rc = hash_geo(n_bits, r_bits, &g);
+  if (rc) return rc;
+  if (batch == 0) return PAB_OK;
+  if (!x || !out) return fail(PAB_EINVAL, "null pointer argument");
+  if (byte_order != PAB_ORDER_LSF && byte_order != PAB_ORDER_MSF)
+    return fail(PAB_EINVAL, "byte_order must be PAB_ORDER_LSF or PAB_ORDER_MSF");
+  if (first_index > ~0ull - batch) return fail(PAB_EINVAL, "block index overflows 64 bits");
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  DevState* ds;
+  if ((rc = ensure_device(device, &ds))) return rc;
+  HostCtx& h = ds->host;
+  std::lock_guard<std::mutex> lk(h.mu);
+  return host_pipeline(x, nullptr, nullptr, n_bits, r_bits, batch, byte_order, master, master_len,
+                       first_index, bench_index, out, h);
 }
 
 int pab_hash_seeded_host(const uint8_t* x, uint64_t n_bits, uint64_t r_bits, uint32_t batch,

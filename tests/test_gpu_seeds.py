@@ -144,6 +144,25 @@ def test_native_seeded_host_pipeline(n, r, B, msf):
     assert _native.hash_seeded_host(x[:3].tobytes(), n, r, 3, 21, first_index=5, order=order) == got[:3 * rb]
 
 
+@pytest.mark.parametrize("n,r,B,msf", [(4_160, 2_001, 2_500, False), (4_099, 17, 1_100, True)])
+def test_native_host_pipeline_with_host_members(n, r, B, msf):
+    # pab_hash_host: the same three-stream pipeline with c and d from the host, several
+    # chunks of 1024 blocks, packed and padded rows
+    order = _native.ORDER_MSF if msf else _native.ORDER_LSF
+    rng = np.random.default_rng(n + B)
+    nb, rb = (n + 7) // 8, (r + 7) // 8
+    x, c, d = (rng.integers(0, 256, size=(B, nb), dtype=np.uint8) for _ in range(3))
+    if n % 8:
+        for a in (x, c, d):
+            a[:, 0 if msf else -1] &= (1 << (n % 8)) - 1
+    c[:, -1 if msf else 0] |= 1
+    got = _native.hash_host(x.tobytes(), c.tobytes(), d.tobytes(), n, r, B, order=order)
+    want = oracle.compress_batch(x.tobytes(), c.tobytes(), d.tobytes(), n, r, B, threads=4, msf=msf)
+    assert got == want
+    assert _native.hash_host(x[:2].tobytes(), c[:2].tobytes(), d[:2].tobytes(), n, r, 2,
+                             order=order) == got[:2 * rb]
+
+
 @pytest.mark.parametrize("protocol", ["run_pa", "bench"])
 def test_engine_hands_synchronous_big_calls_to_the_native_pipeline(protocol):
     # hash_seeded_host: a synchronous call of >= kExclusiveMin packed host blocks is one C call
